@@ -1,0 +1,99 @@
+/*
+ * hb200.h — C ABI of libhb200.so, the B200 (sm_100a) kernels behind the
+ * hybridbench work-partitioned hot path (arXiv 1303.2171).
+ *
+ * Every entry point replaces the DeviceB side of one reference `run_part`
+ * (or the equivalent side function) in /root/reference/pkg/src/hybridbench/.
+ * The citation above each declaration names the reference interface it
+ * replaces.  The Python package paper_1303_2171_b200 binds these through
+ * ctypes.CDLL (which releases the GIL, so the two `run_workshared` threads
+ * really overlap, cf. worksharing.py:317-320); INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  `stream` is a cudaStream_t passed as
+ *    void* (NULL = the legacy default stream of the current device).
+ *  - `flags & HB_DEVICE_PTRS`: every data pointer is a device pointer on the
+ *    current device.  Otherwise every data pointer is a HOST pointer (pinned
+ *    or pageable) and the library stages it through its own device buffers;
+ *    host↔device copies then happen inside the call.
+ *  - `flags & HB_ASYNC` (device pointers only): return without synchronising
+ *    the stream.  Checks that need a device→host read are then skipped.
+ *  - Return value: HB_OK, or an HB_E* code; hb_last_error() gives a
+ *    thread-local message.  The Python layer maps HB_EINVAL → ValueError,
+ *    HB_ESTRUCT → StructuralError, everything else → HybridBenchError
+ *    (reference hierarchy: errors.py:10-49).
+ */
+#ifndef HB200_H
+#define HB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_EINVAL 1   /* argument / domain error      -> ValueError          */
+#define HB_ESTRUCT 2  /* malformed structure          -> StructuralError     */
+#define HB_ECUDA 3    /* CUDA runtime failure         -> HybridBenchError    */
+#define HB_ENOMEM 4   /* device allocation failed     -> HybridBenchError    */
+#define HB_ENOSYS 5   /* not supported on this device -> HybridBenchError    */
+
+#define HB_DEVICE_PTRS 1
+#define HB_ASYNC 2
+
+/* element type codes for the histogram input (numpy dtype.kind/itemsize) */
+#define HB_U8 1
+#define HB_I8 2
+#define HB_U16 3
+#define HB_I16 4
+#define HB_U32 5
+#define HB_I32 6
+#define HB_U64 7
+#define HB_I64 8
+
+/* ------------------------------------------------------------------ runtime */
+int hb_version(void);
+const char* hb_last_error(void);
+/* Number of visible CUDA devices (0 if the driver has none). */
+int hb_device_count(int* count);
+/* SM count of the current device (grid sizing is a multiple of it). */
+int hb_sm_count(int* count);
+/* Synchronise `stream` and surface any pending CUDA error. */
+int hb_stream_sync(void* stream);
+/* Release cached device staging buffers of the current device. */
+int hb_trim(void);
+
+/* ---------------------------------------------------------------- generators
+ * Device-side restatement of rng.py:45-51 (`splitmix64_array`): draw k
+ * (1-based, k = k0+1 .. k0+n) of the stream `seed`, transformed:
+ *   HB_GEN_RAW  u64 draw                         (splitmix64_array)
+ *   HB_GEN_LOW8 u8  draw & 255                   (gen_hist_data / gen_image,
+ *                                                 datasets.py:33-34, 104-106)
+ *   HB_GEN_HI32 u32 draw >> 32                   (gen_sort_data, datasets.py:28-30)
+ *   HB_GEN_MOD  i64 draw % bound                 (uniform_ints, rng.py:65-67)
+ * `out` is a device pointer.  Bit-identical to the reference for every k.   */
+#define HB_GEN_RAW 0
+#define HB_GEN_LOW8 1
+#define HB_GEN_HI32 2
+#define HB_GEN_MOD 3
+int hb_gen_splitmix(uint64_t seed, uint64_t k0, int64_t n, int kind, uint64_t bound,
+                    void* out, void* stream);
+
+/* ---------------------------------------------------------------- histogram
+ * Replaces HistogramWorkload.run_part (kernels_regular.py:149-154): the bin
+ * counts of `data[0:n]` (element type `dtype`), bin b = element value.
+ * `bins_out` receives bin_count uint64 counts (ADDED to it when
+ * flags & HB_ACCUMULATE, overwritten otherwise).  Elements outside
+ * [0, bin_count) → HB_EINVAL, the reference's ValueError
+ * (kernels_regular.py:137-138).  Supports 1 <= bin_count <= 49152.       */
+#define HB_ACCUMULATE 4
+int hb_hist(const void* data, int dtype, int64_t n, int32_t bin_count, uint64_t* bins_out,
+            int flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HB200_H */

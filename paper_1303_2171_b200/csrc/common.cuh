@@ -1,0 +1,104 @@
+// common.cuh — shared plumbing for libhb200.so: error reporting, stream-ordered
+// staging buffers for host-pointer calls, launch geometry, PTX load helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/hb200.h"
+
+namespace hb {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+
+#define HB_CUDA_TRY(expr)                                                            \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::hb::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return _e == cudaErrorMemoryAllocation ? HB_ENOMEM : HB_ECUDA;                 \
+    }                                                                                \
+  } while (0)
+
+#define HB_TRY(expr)            \
+  do {                          \
+    int _rc = (expr);           \
+    if (_rc != HB_OK) return _rc; \
+  } while (0)
+
+#define HB_CHECK_ARG(cond, ...)      \
+  do {                               \
+    if (!(cond)) {                   \
+      ::hb::set_error(__VA_ARGS__);  \
+      return HB_EINVAL;              \
+    }                                \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ device info
+struct DeviceInfo {
+  int id = -1;
+  int sms = 0;
+  size_t smem_optin = 0;
+};
+int device_info(DeviceInfo* out);  // cached per device
+
+// ------------------------------------------------------------------ buffers
+// A device buffer that is either borrowed (caller passed a device pointer)
+// or owned (stream-ordered allocation from the device's default mem pool,
+// whose release threshold we raise so repeated calls reuse memory).
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  bool owned = false;
+  cudaStream_t stream = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (owned && ptr) cudaFreeAsync(ptr, stream);
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
+int alloc(DevBuf* b, size_t bytes, cudaStream_t s);
+// Stage a caller buffer: borrow it when `device`, else allocate + H2D copy.
+int stage_in(DevBuf* b, const void* src, size_t bytes, bool device, cudaStream_t s);
+// Output buffer: borrow when `device`, else allocate (no copy).
+int stage_out(DevBuf* b, void* dst, size_t bytes, bool device, cudaStream_t s);
+int copy_out(void* dst, const DevBuf& b, size_t bytes, bool device, cudaStream_t s);
+int finish(int flags, cudaStream_t s);  // sync unless HB_ASYNC, surface errors
+int check_launch();
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+// splitmix64 finaliser of draw k (1-based) of stream `seed` (rng.py:45-51).
+__host__ __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t k) {
+  uint64_t z = seed + k * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace hb

@@ -1,0 +1,452 @@
+"""Benchmark driver for the B200 work-partitioned hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload hist|…|all]
+                    [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  At N=1 the headline workload is BASELINE.json
+configs[1] — 256-bin histogram over 2^30 uint8 elements — and every other
+configured workload is measured in the same run under "workloads".  A step is
+one pass of the hot path over one batch of synthetic input already resident
+in HBM (`value`); `e2e` is the same metric through the public drop-in API
+(`hybrid_histogram(...)` on pinned host buffers, H2D + D2H inside the timed
+region).  Under torchrun (N>1) every rank holds its own shard (weak scaling)
+and the per-step merge is the workload's real collective (NCCL).
+
+`--impl reference` times the reference's own CPU algorithm (the numpy
+restatement under oracle/, the reference being pure Python) on the host
+cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
+METRIC = "per-workload throughput (SpMV GFLOP/s, sort Mkeys/s) and HBM-roofline fraction"
+
+
+# ---------------------------------------------------------------- utilities
+def hbm_peak() -> tuple[float, str]:
+    try:
+        return float(json.loads(PEAKS_FILE.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_of(kernel: str):
+    try:
+        return json.loads(TRAFFIC_FILE.read_text()).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Polls NVML (SM clock + clock-event reasons) on a thread; `window()`
+    returns the samples that fall inside [t0, t1]."""
+
+    REASONS = {
+        "hw_slowdown": 0x8,
+        "hw_thermal_slowdown": 0x40,
+        "sw_thermal_slowdown": 0x20,
+        "sw_power_cap": 0x4,
+        "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index: int):
+        self.samples: list[tuple[float, int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self) -> None:
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((time.perf_counter(), mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(timeout=1)
+
+    def summary(self, t0: float, t1: float) -> dict:
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        window = "timed"
+        if not inside:  # region shorter than the polling period: nearest samples
+            inside = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:5]
+            window = "adjacent"
+        reasons = set()
+        for _, _, rs in inside:
+            for name, bit in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        mhz = [m for _, m, _ in inside]
+        return {
+            "sm_mhz": statistics.median(mhz) if mhz else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(reasons),
+            "samples": len(mhz),
+            "window": window,
+        }
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- workloads
+class HistBench:
+    """BASELINE configs[1]: 256-bin histogram over 2^30 uint8 (per GPU)."""
+
+    name = "hist"
+    unit = "Gelem/s"
+    kernel = "hist_striped_kernel"
+
+    def __init__(self, n: int = 1 << 30, bins: int = 256, seed: int = 42):
+        self.n, self.bins, self.seed = n, bins, seed
+
+    def config(self):
+        return {"workload": f"hist: 256-bin histogram over 2^{self.n.bit_length() - 1} uint8 per GPU",
+                "n_per_gpu": self.n, "bins": self.bins, "seed": self.seed,
+                "input": "gen_hist_data(n, 42) low byte (splitmix64, device-generated)",
+                "l2": "input (1 GiB) > L2 (126 MB): no flush needed"}
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_1303_2171_b200 import _lib
+        from paper_1303_2171_b200.rng import device_splitmix
+
+        self.x = torch.empty(self.n, dtype=torch.uint8, device="cuda")
+        device_splitmix(self.x, self.seed, _lib.HB_GEN_LOW8, k0=rank * self.n)
+        self.out = torch.empty(self.bins, dtype=torch.int64, device="cuda")
+        self.world = world
+
+    def step(self):
+        from paper_1303_2171_b200.kernels_regular import gpu_histogram
+
+        gpu_histogram(self.x, self.bins, self.out, asynchronous=True)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.out)
+        return 1  # libhb200 kernels launched
+
+    def units_per_step(self):
+        return self.n
+
+    def bytes_per_launch(self):
+        return self.n * 1 + self.bins * 8
+
+    def verify(self):
+        import torch
+
+        from oracle import hist as ohist
+
+        # sampled check on the host: the first 2^24 elements vs the oracle
+        m = 1 << 24
+        part = self.x[:m]
+        got = torch.empty(self.bins, dtype=torch.int64, device="cuda")
+        from paper_1303_2171_b200.kernels_regular import gpu_histogram
+
+        gpu_histogram(part, self.bins, got)
+        host = part.cpu().numpy()
+        ok = np.array_equal(got.cpu().numpy(), ohist.side_counts(host, self.bins, 1))
+        full = int(self.out.sum().item()) == self.n * self.world
+        return bool(ok and full)
+
+    # end-to-end through the public drop-in API, pinned host buffers
+    def e2e_setup(self):
+        import torch
+
+        self.host = torch.empty(self.n, dtype=torch.uint8, pin_memory=True)
+        self.host.copy_(self.x)
+        self.host_np = self.host.numpy()
+        from paper_1303_2171_b200.platform import Platform
+        from paper_1303_2171_b200.worksharing import WorkShare
+
+        self.platform = Platform.build(1.0, 3.0)
+        self.share = WorkShare.manual(0.0)
+
+    def e2e_step(self):
+        from paper_1303_2171_b200.kernels_regular import hybrid_histogram
+
+        res = hybrid_histogram(self.host_np, self.bins, self.platform, self.share)
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            t = torch.from_numpy(res.bins).cuda()
+            dist.all_reduce(t)
+        return res
+
+    def e2e_bytes(self):
+        return self.n, self.bins * 8
+
+    # CPU baseline: the reference algorithm (oracle port) on a bounded sample
+    def cpu_sample(self, budget_s: float):
+        from oracle import hist as ohist
+
+        m = min(self.n, 1 << 28)
+        host = self.x[:m].cpu().numpy()
+        fn = lambda: ohist.hybrid(host, self.bins, 0.25)  # noqa: E731
+        return fn, m, f"{m} uint8 elements of the same stream (2^{m.bit_length() - 1}), formula share 0.25, 2 sides x 4 workers"
+
+    def cpu_cores(self):
+        return 2
+
+
+WORKLOADS = {"hist": HistBench}
+
+
+# ---------------------------------------------------------------- drivers
+def time_cpu(fn, reps: int, warm: int = 1):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def run_reference(args, wl) -> dict:
+    """--impl reference: the reference CPU algorithm on the host cores."""
+    import torch
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return {}
+    torch.cuda.set_device(local) if torch.cuda.is_available() else None
+    wl.setup(0, 1)
+    fn, units, sample = wl.cpu_sample(30.0)
+    ts = time_cpu(fn, args.steps, warm=args.warmup)
+    t = statistics.median(ts)
+    val = units / t / 1e9 if wl.unit.startswith("G") else units / t / 1e6
+    return {
+        "metric": METRIC,
+        "impl": "reference",
+        "value": val,
+        "unit": wl.unit,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic",
+        "config": wl.config(),
+        "cpu_baseline": {"value": val, "unit": wl.unit, "cores": wl.cpu_cores(), "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": wl.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def measure(args, wl, rank, world, with_cpu: bool) -> dict:
+    import torch
+
+    wl.setup(rank, world)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        for _ in range(args.warmup):
+            wl.step()
+        torch.cuda.synchronize()
+        barrier(world)
+        launches = 0
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        start.record(stream)
+        for _ in range(args.steps):
+            launches += wl.step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        barrier(world)
+        ms = start.elapsed_time(end) / args.steps
+        ms = max_over_ranks(ms, world)
+        clk = clocks.summary(t0, t1)
+    ok = wl.verify()
+
+    # end-to-end through the public API (host pinned buffers)
+    wl.e2e_setup()
+    for _ in range(max(1, args.warmup)):
+        wl.e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0 = time.perf_counter()
+    for _ in range(args.steps):
+        wl.e2e_step()
+    torch.cuda.synchronize()
+    e_s = (time.perf_counter() - e0) / args.steps
+    barrier(world)
+    e_s = max_over_ranks(e_s, world)
+
+    scale = 1e9 if wl.unit.startswith("G") else 1e6
+    value = wl.units_per_step() * world / (ms / 1e3) / scale
+    peak, peak_src = hbm_peak()
+    achieved = wl.bytes_per_launch() / (ms / 1e3) / 1e9
+    h2d, d2h = wl.e2e_bytes()
+    res = {
+        "value": value,
+        "unit": wl.unit,
+        "ms_per_step": ms,
+        "parity": ok,
+        "gpu_launches": launches,
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic_of(wl.kernel),
+            "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": wl.bytes_per_launch(),
+            "kernel": wl.kernel,
+        },
+        "e2e": {
+            "value": wl.units_per_step() * world / e_s / scale,
+            "unit": wl.unit,
+            "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+            "ms_per_step": e_s * 1e3,
+            "api": "public drop-in entry point on pinned host buffers",
+        },
+        "clocks": clk,
+        "config": wl.config(),
+    }
+    if with_cpu and rank == 0:
+        fn, units, sample = wl.cpu_sample(20.0)
+        ts = time_cpu(fn, 1, warm=0)
+        cv = units / min(ts) / scale
+        res["cpu_baseline"] = {"value": cv, "unit": wl.unit, "cores": wl.cpu_cores(), "kind": "port", "sample": sample}
+    return res
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="hist", choices=sorted(WORKLOADS) + ["all"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = dist_env()
+    headline = "hist" if args.workload == "all" else args.workload
+
+    if args.impl == "reference":
+        out = run_reference(args, WORKLOADS[headline]())
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1303_2171_b200.gpu import require_gpu
+
+    require_gpu()
+
+    head = measure(args, WORKLOADS[headline](), rank, world, with_cpu=(world == 1 and not args.no_cpu))
+    others = {}
+    if args.workload == "all":
+        for name, cls in WORKLOADS.items():
+            if name != headline:
+                others[name] = measure(args, cls(), rank, world, with_cpu=(world == 1 and not args.no_cpu))
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": head["value"],
+            "unit": head["unit"],
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u8",
+            "data": "synthetic (splitmix64 streams of the reference generators, seed 42)",
+            "config": dict(head["config"], parallelism=f"shard{world}"),
+            "roofline": head["roofline"],
+            "e2e": head["e2e"],
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
+            "parity": head["parity"],
+        }
+        if "cpu_baseline" in head:
+            line["cpu_baseline"] = head["cpu_baseline"]
+        if others:
+            line["workloads"] = others
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,135 @@
+"""Host-side plumbing between numpy / torch arrays and the C ABI.
+
+A *buffer* handed to a `hb_*` call is either a host array (numpy; the
+library stages it through device memory inside the call) or a CUDA tensor
+(torch, device-resident; the call passes `HB_DEVICE_PTRS` and works in place
+on the caller's stream).  PyTorch is only plumbing here — device memory,
+streams and `torch.distributed`; every computation is a libhb200 kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Any
+
+import numpy as np
+
+from . import _lib
+
+try:  # torch is optional for host-array use; required for device-resident use
+    import torch
+except Exception:  # pragma: no cover - torch is in the image
+    torch = None  # type: ignore[assignment]
+
+
+def is_device_array(x: Any) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def require_gpu() -> None:
+    """Fail loudly when the GPU share cannot run (no silent CPU fallback)."""
+    _lib.load()
+    if _lib.device_count() < 1:
+        from .errors import HybridBenchError
+
+        raise HybridBenchError("no CUDA device visible: the DeviceB (GPU) share cannot run")
+
+
+def current_stream_handle(x: Any = None) -> int:
+    """cudaStream_t of torch's current stream (0 = legacy default stream)."""
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        dev = x.device if is_device_array(x) else None
+        return int(torch.cuda.current_stream(dev).cuda_stream)
+    return 0
+
+
+_TORCH_TO_NP = {}
+if torch is not None:
+    _TORCH_TO_NP = {
+        torch.uint8: np.dtype(np.uint8),
+        torch.int8: np.dtype(np.int8),
+        torch.int16: np.dtype(np.int16),
+        torch.int32: np.dtype(np.int32),
+        torch.int64: np.dtype(np.int64),
+        torch.float32: np.dtype(np.float32),
+        torch.float64: np.dtype(np.float64),
+    }
+    for _name in ("uint16", "uint32", "uint64"):
+        if hasattr(torch, _name):
+            _TORCH_TO_NP[getattr(torch, _name)] = np.dtype(_name)
+
+
+@dataclass
+class Buf:
+    """A raw view of an array for the C ABI."""
+
+    ptr: int
+    size: int  # elements
+    dtype: np.dtype
+    device: bool
+    owner: Any  # keeps the memory alive for the duration of the call
+
+    @property
+    def nbytes(self) -> int:
+        return self.size * self.dtype.itemsize
+
+    @property
+    def code(self) -> int:
+        return _lib.DTYPE_CODES[self.dtype.str[1:]] if self.dtype.str[1:] in _lib.DTYPE_CODES else 0
+
+
+def buf(x: Any, dtype: Any = None) -> Buf:
+    """View `x` (numpy array or CUDA tensor) as a C-ABI buffer.  Host arrays
+    are made C-contiguous (and cast to `dtype` when given); device tensors
+    must already be contiguous and of the right dtype."""
+    if is_device_array(x):
+        if not x.is_contiguous():
+            x = x.contiguous()
+        dt = _TORCH_TO_NP.get(x.dtype)
+        if dt is None:
+            raise TypeError(f"unsupported tensor dtype {x.dtype}")
+        if dtype is not None and np.dtype(dtype) != dt:
+            raise TypeError(f"expected a {np.dtype(dtype)} tensor, got {x.dtype}")
+        return Buf(x.data_ptr(), x.numel(), dt, True, x)
+    arr = np.asarray(x)
+    if dtype is not None and arr.dtype != np.dtype(dtype):
+        arr = arr.astype(dtype)
+    arr = np.ascontiguousarray(arr)
+    return Buf(arr.ctypes.data if arr.size else 0, arr.size, arr.dtype, False, arr)
+
+
+def out_like(device: bool, shape: Any, dtype: Any, ref: Any = None) -> Any:
+    """Allocate an output on the same side as the input."""
+    if device:
+        return torch.empty(shape, dtype=_np_to_torch(np.dtype(dtype)), device=ref.device if ref is not None else "cuda")
+    return np.empty(shape, dtype=dtype)
+
+
+def _np_to_torch(dt: np.dtype):
+    for k, v in _TORCH_TO_NP.items():
+        if v == dt:
+            return k
+    raise TypeError(f"no torch dtype for {dt}")
+
+
+def flags_for(*bufs: Buf, asynchronous: bool = False) -> int:
+    """HB_DEVICE_PTRS when every buffer is device memory; mixing is refused."""
+    kinds = {b.device for b in bufs if b.size or b.ptr}
+    if len(kinds) > 1:
+        raise ValueError("mixing host arrays and CUDA tensors in one call is not supported")
+    dev = kinds == {True}
+    f = _lib.HB_DEVICE_PTRS if dev else 0
+    if asynchronous and dev:
+        f |= _lib.HB_ASYNC
+    return f
+
+
+def to_host(x: Any) -> np.ndarray:
+    if is_device_array(x):
+        return x.cpu().numpy()
+    return np.asarray(x)
+
+
+def vp(ptr: int) -> ctypes.c_void_p:
+    return ctypes.c_void_p(ptr)

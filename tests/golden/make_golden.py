@@ -1,0 +1,127 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE
+implementation (hybridbench, imported from /root/reference/pkg/src in the dev
+container).  The GPU box has no /root/reference; the tests read only the
+committed .npz files.  Re-run with:  python tests/golden/make_golden.py
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+
+
+def main() -> None:
+    sys.path.insert(0, str(REF))
+    from hybridbench import datasets, rng
+    from hybridbench.kernels_irregular import (
+        CsrMatrix,
+        LinkedListArr,
+        list_rank_with_stats,
+        spmv_hybrid,
+        spmv_preprocess,
+    )
+    from hybridbench.kernels_regular import (
+        Image,
+        bilateral_rows,
+        build_bilateral_lut,
+        hybrid_bilateral,
+        hybrid_histogram,
+        sample_sort_hybrid,
+    )
+    from hybridbench.platform import Platform
+    from hybridbench.worksharing import WorkShare
+
+    p13 = Platform.build(1.0, 3.0)
+    shares = [i / 10 for i in range(11)]
+
+    # ------------------------------------------------------------- rng
+    g = {}
+    for seed in (0, 42, 12345, 0xDEADBEEF):
+        g[f"splitmix_{seed}"] = rng.splitmix64_array(seed, 64)
+    g["mix_seed"] = np.array([rng.mix_seed(s, t) for s in (0, 1, 42) for t in (0, 1, 2, 3, 0x5EED, 0xDEC0)], dtype=np.uint64)
+    g["uniform_floats_7"] = rng.uniform_floats(7, 32)
+    g["uniform_ints_9"] = rng.uniform_ints(9, 32, 1000)
+    np.savez_compressed(OUT / "rng.npz", **g)
+
+    # ------------------------------------------------------------- hist
+    h = {}
+    for i, (n, seed, bins) in enumerate([(20_000, 11, 256), (3000, 3, 32), (4096, 5, 64), (1_000_000, 42, 256)]):
+        data = datasets.gen_hist_data(n, seed, bins)
+        h[f"data_{i}"] = data.astype(np.uint8) if bins <= 256 else data
+        h[f"meta_{i}"] = np.array([n, seed, bins])
+        h[f"bins_{i}"] = np.stack([hybrid_histogram(data, bins, p13, WorkShare.manual(s)).bins for s in shares])
+    np.savez_compressed(OUT / "hist.npz", **h)
+
+    # ------------------------------------------------------------- sort
+    s = {}
+    cases = [
+        ("uar50k", datasets.gen_sort_data(50_000, 1)),
+        ("dups", datasets.gen_sort_data(30_000, 42) % 5000),
+        ("rev", np.arange(3000)[::-1].copy()),
+        ("tiny", datasets.gen_sort_data(1500, 2)),
+        ("const", np.full(5000, 9, dtype=np.int64)),
+    ]
+    for name, data in cases:
+        s[f"{name}_data"] = data
+        rows = []
+        for sh in (0.0, 0.25, 0.5, 1.0):
+            out, wa, wb = sample_sort_hybrid(data, p13, share=WorkShare.manual(sh))
+            assert np.array_equal(out, np.sort(data))
+            rows.append([sh, wa, wb])
+        _, wa, wb = sample_sort_hybrid(data, p13)  # formula share 0.25
+        rows.append([-1.0, wa, wb])
+        s[f"{name}_work"] = np.array(rows)
+    np.savez_compressed(OUT / "sort.npz", **s)
+
+    # ------------------------------------------------------------- spmv
+    m = {}
+    for i, (rows_, density, seed) in enumerate([(50, 0.1, 3), (30, 0.15, 5), (2000, 0.004, 42), (36, 0.12, 80)]):
+        mat = datasets.gen_csr(rows_, rows_, seed, density)
+        x = 2.0 * rng.uniform_floats(rng.mix_seed(seed, 0xDEC0), rows_) - 1.0
+        m[f"ptr_{i}"], m[f"col_{i}"], m[f"val_{i}"], m[f"x_{i}"] = mat.row_ptr, mat.col_idx, mat.values, x
+        prep = spmv_preprocess(mat, p13)
+        m[f"perm_{i}"] = prep.perm
+        m[f"split_{i}"] = np.array([prep.split_row] + [spmv_preprocess(mat, p13, WorkShare.manual(sh)).split_row for sh in shares])
+        m[f"y_{i}"] = spmv_hybrid(prep, x)
+    ident = CsrMatrix.identity(100)
+    m["identity100_split"] = np.array([spmv_preprocess(ident, p13).split_row])
+    np.savez_compressed(OUT / "spmv.npz", **m)
+
+    # ------------------------------------------------------------- bilateral
+    b = {}
+    for i, (side, seed, radius, ss, sr) in enumerate([(24, 8, 2, 2.0, 30.0), (64, 4, 3, 2.5, 35.0), (40, 42, 5, 2.5, 40.0), (33, 7, 7, 3.5, 40.0)]):
+        img = datasets.gen_image(side, seed)
+        lut = build_bilateral_lut(radius, ss, sr)
+        b[f"img_{i}"] = img.pixels
+        b[f"meta_{i}"] = np.array([side, seed, radius, ss, sr])
+        b[f"spatial_{i}"], b[f"range_{i}"] = lut.spatial_weights, lut.range_weights
+        b[f"out_{i}"] = hybrid_bilateral(img, lut, p13).pixels
+        b[f"strip_{i}"] = bilateral_rows(img.pixels, lut, side // 3, side // 3 + 5)
+    rect = Image(datasets.gen_image(48, 3).pixels[:20, :].copy())
+    lut = build_bilateral_lut(3, 2.0, 25.0)
+    b["rect_img"], b["rect_out"] = rect.pixels, hybrid_bilateral(rect, lut, p13).pixels
+    np.savez_compressed(OUT / "bilateral.npz", **b)
+
+    # ------------------------------------------------------------- list ranking
+    lr = {}
+    for i, (n, seed, rseed) in enumerate([(10_000, 42, 7), (500, 0, 0), (1000, 3, 3), (4097, 11, 5), (2, 1, 1), (1, 1, 1)]):
+        if n == 1:
+            lst = LinkedListArr(np.array([-1]), 0)
+        else:
+            lst = datasets.gen_list(n, seed)
+        ranks, st = list_rank_with_stats(lst, p13, rseed)
+        lr[f"succ_{i}"], lr[f"head_{i}"], lr[f"seed_{i}"] = lst.succ, np.array([lst.head]), np.array([rseed])
+        lr[f"rank_{i}"] = ranks
+        lr[f"stats_{i}"] = np.array([st.fis_rounds, st.reduced_size, st.removed_total, st.sublist_count])
+        lr[f"sizes_{i}"] = np.array(st.round_sizes, dtype=np.int64)
+    np.savez_compressed(OUT / "listrank.npz", **lr)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

@@ -250,7 +250,102 @@ class HistBench:
         return 2
 
 
-WORKLOADS = {"hist": HistBench}
+class SpmvBench:
+    """BASELINE configs[0]: CSR SpMV, 1M x 1M, ~16 nnz/row, fp64 (gen_csr seed 42,
+    density 1.6e-5), rows nnz-sorted by spmv_preprocess; one step = y = A x
+    over all rows with the inverse permutation fused into the store."""
+
+    name = "spmv"
+    unit = "GFLOP/s"
+    kernel = "spmv_seq_kernel"
+
+    def __init__(self, rows: int = 1_000_000, density: float = 1.6e-5, seed: int = 42):
+        self.rows, self.density, self.seed = rows, density, seed
+
+    def config(self):
+        return {"workload": f"spmv: CSR {self.rows}x{self.rows}, density {self.density} (~16 nnz/row), fp64, bit-exact row sums",
+                "rows": self.rows, "nnz": int(self.nnz), "seed": self.seed,
+                "input": "gen_csr(rows, rows, 42, 1.6e-5) + x = 2*uniform_floats(mix_seed(42,0xDEC0))-1",
+                "l2": "matrix (204 MB) > L2 (126 MB); x (8 MB) L2-resident by design"}
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_1303_2171_b200.datasets import gen_csr
+        from paper_1303_2171_b200.kernels_irregular import CsrMatrix, spmv_preprocess
+        from paper_1303_2171_b200.platform import Platform
+        from paper_1303_2171_b200.rng import mix_seed, uniform_floats
+        from paper_1303_2171_b200.worksharing import WorkShare
+
+        ptr, col, val = gen_csr(self.rows, self.rows, self.seed, self.density)
+        self.m = CsrMatrix(self.rows, self.rows, ptr, col, val)
+        self.nnz = self.m.nnz
+        self.x_host = 2.0 * uniform_floats(mix_seed(self.seed, 0xDEC0), self.rows) - 1.0
+        self.platform = Platform.build(1.0, 3.0)
+        self.prep = spmv_preprocess(self.m, self.platform, WorkShare.manual(0.0))
+        self.dm = self.prep.permuted.to_device(np.int32)
+        self.x = torch.from_numpy(self.x_host).cuda()
+        self.perm = torch.from_numpy(np.asarray(self.prep.perm, dtype=np.int32)).cuda()
+        self.y = torch.empty(self.rows, dtype=torch.float64, device="cuda")
+        self.world = world
+
+    def step(self):
+        from paper_1303_2171_b200.kernels_irregular import gpu_spmv
+
+        gpu_spmv(self.dm, self.x, 0, self.rows, y=self.y, perm=self.perm, asynchronous=True)
+        return 1
+
+    def units_per_step(self):
+        return 2 * self.nnz  # flops
+
+    def bytes_per_launch(self):
+        r = self.rows
+        return 12 * self.nnz + 4 * (r + 1) + 8 * r + 8 * r + 4 * r  # val+col, row_ptr, x, y, perm
+
+    def verify(self):
+        from oracle import spmv as ospmv
+
+        p = self.prep.permuted
+        want = ospmv.hybrid(self.prep.perm, (p.row_ptr, p.col_idx, p.values), 0, self.x_host)
+        return bool(np.array_equal(self.y.cpu().numpy().view(np.uint64), want.view(np.uint64)))
+
+    def e2e_setup(self):
+        import torch
+
+        from paper_1303_2171_b200.kernels_irregular import CsrMatrix, SpmvPrep
+
+        def pinned(a):
+            t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+            t.numpy()[...] = a
+            return t.numpy()
+
+        p = self.prep.permuted
+        self.hprep = SpmvPrep(CsrMatrix(p.rows, p.cols, pinned(p.row_ptr), pinned(p.col_idx), pinned(p.values)),
+                              self.prep.perm, 0)
+        self.hx = pinned(self.x_host)
+
+    def e2e_step(self):
+        from paper_1303_2171_b200.kernels_irregular import spmv_hybrid
+
+        return spmv_hybrid(self.hprep, self.hx)
+
+    def e2e_bytes(self):
+        p = self.prep.permuted
+        return (p.row_ptr.nbytes + p.col_idx.nbytes + p.values.nbytes + self.x_host.nbytes), 8 * self.rows
+
+    def cpu_sample(self, budget_s: float):
+        from oracle import spmv as ospmv
+
+        perm, permuted, _ = ospmv.preprocess(self.m.row_ptr, self.m.col_idx, self.m.values, 1.0, 3.0, None)
+        split = ospmv.workload_split(permuted[0], 0.25)
+        fn = lambda: ospmv.hybrid(perm, permuted, split, self.x_host)  # noqa: E731
+        return fn, 2 * self.nnz, "full 1M-row matrix, one SpMV (prep excluded), formula share 0.25, 2 threads"
+
+    def cpu_cores(self):
+        return 2
+
+
+WORKLOADS = {"hist": HistBench, "spmv": SpmvBench}
 
 
 # ---------------------------------------------------------------- drivers
@@ -277,7 +372,7 @@ def run_reference(args, wl) -> dict:
     fn, units, sample = wl.cpu_sample(30.0)
     ts = time_cpu(fn, args.steps, warm=args.warmup)
     t = statistics.median(ts)
-    val = units / t / 1e9 if wl.unit.startswith("G") else units / t / 1e6
+    val = units / t / (1e9 if wl.unit.startswith("G") else 1e6)
     return {
         "metric": METRIC,
         "impl": "reference",

@@ -93,6 +93,30 @@ int hb_gen_splitmix(uint64_t seed, uint64_t k0, int64_t n, int kind, uint64_t bo
 int hb_hist(const void* data, int dtype, int64_t n, int32_t bin_count, uint64_t* bins_out,
             int flags, void* stream);
 
+
+/* --------------------------------------------------------------------- SpMV
+ * Replaces _csr_range_matvec / SpmvWorkload.run_part (kernels_irregular.py:
+ * 206-211, 250-251): y = A[row0:row1] x over a CSR whose row_ptr entries are
+ * absolute offsets into col_idx/values.  Index arrays are HB_I32 or HB_I64.
+ *   perm == NULL: y[i-row0] = row i's sum         (the y_perm slice)
+ *   perm != NULL: y[perm[i]] = row i's sum        (fused inverse permutation,
+ *                                                  SpmvWorkload.merge :253-257)
+ * mode HB_SPMV_SEQ: bit-identical to the reference (rounded products, rows
+ * summed left to right, no FMA).  HB_SPMV_WARP: warp tree reduction,
+ * within 1e-9 relative.  Host-pointer calls stage only the row range.     */
+#define HB_SPMV_SEQ 0
+#define HB_SPMV_WARP 1
+int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
+                const double* values, int64_t row0, int64_t row1, int64_t cols, const double* x,
+                const void* perm, int perm_code, double* y, int mode, int flags, void* stream);
+
+/* CsrMatrix invariants (kernels_irregular.py:44-60) checked on the device:
+ * *flags_out |= 1 bad row_ptr ends, 2 decreasing row_ptr, 4 column out of
+ * range, 8 columns not strictly increasing within a row.                   */
+int hb_csr_validate(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
+                    int64_t rows, int64_t nnz, int64_t cols, uint32_t* flags_out, int flags,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ HB_ASYNC = 2
 HB_ACCUMULATE = 4
 
 HB_GEN_RAW, HB_GEN_LOW8, HB_GEN_HI32, HB_GEN_MOD = range(4)
+HB_SPMV_SEQ, HB_SPMV_WARP = 0, 1
 
 # numpy dtype.str (sans byte order) -> element code of include/hb200.h
 DTYPE_CODES = {"u1": 1, "i1": 2, "u2": 3, "i2": 4, "u4": 5, "i4": 6, "u8": 7, "i8": 8}
@@ -43,6 +44,8 @@ _SIGNATURES: dict[str, list] = {
     "hb_trim": [],
     "hb_gen_splitmix": [_u64, _u64, _i64, _int, _u64, _vp, _vp],
     "hb_hist": [_vp, _int, _i64, _i32, _vp, _int, _vp],
+    "hb_spmv_csr": [_vp, _int, _vp, _int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _vp, _int, _int, _vp],
+    "hb_csr_validate": [_vp, _int, _vp, _int, _i64, _i64, _i64, _vp, _int, _vp],
 }
 
 _lock = threading.Lock()

@@ -75,8 +75,10 @@ def gpu_histogram(part: Any, bin_count: int, out: Any = None, *, asynchronous: b
     Host input → int64 numpy counts.  CUDA-tensor input → counts written to
     `out` (int64 CUDA tensor, allocated when None) and returned; with
     `asynchronous=True` nothing is synchronised (for graph capture/timing)."""
-    require_gpu()
     b = buf(part)
+    if b.size or b.device:
+        require_gpu()
+    _lib.load()
     if b.code == 0:
         raise TypeError(f"histogram input must be an integer array, got {b.dtype}")
     if b.device:

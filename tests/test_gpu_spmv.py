@@ -1,0 +1,135 @@
+"""SpMV GPU parity through the C ABI: bit-exact against the reference's own
+outputs (golden) and the oracle's sequential row sums; mirrors the
+reference's tests/test_kernels_irregular.py:70-128 and acceptance :153-160."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import datasets as ods
+from oracle import rng as orng
+from oracle import spmv as ospmv
+from paper_1303_2171_b200.errors import StructuralError
+from paper_1303_2171_b200.kernels_irregular import (
+    CsrMatrix,
+    SpmvPrep,
+    SpmvWorkload,
+    gpu_spmv,
+    spmv_hybrid,
+    spmv_preprocess,
+)
+from paper_1303_2171_b200.platform import Platform
+from paper_1303_2171_b200.worksharing import WorkShare, run_workshared
+
+pytestmark = pytest.mark.gpu
+SHARES = [i / 10 for i in range(11)]
+
+
+def bits(a):
+    return np.asarray(a, dtype=np.float64).view(np.uint64)
+
+
+def test_golden_bit_exact_all_shares(platform13):
+    g = golden("spmv")
+    for i in range(4):
+        m = CsrMatrix(len(g[f"ptr_{i}"]) - 1, len(g[f"x_{i}"]), g[f"ptr_{i}"], g[f"col_{i}"], g[f"val_{i}"])
+        x = g[f"x_{i}"]
+        prep = spmv_preprocess(m, platform13)
+        assert np.array_equal(prep.perm, g[f"perm_{i}"]) and prep.split_row == g[f"split_{i}"][0]
+        assert np.array_equal(bits(spmv_hybrid(prep, x)), bits(g[f"y_{i}"]))
+        for j, sh in enumerate(SHARES):
+            p = spmv_preprocess(m, platform13, WorkShare.manual(sh))
+            assert p.split_row == g[f"split_{i}"][j + 1]
+            assert np.array_equal(bits(spmv_hybrid(p, x)), bits(g[f"y_{i}"]))
+        # device-resident matrix and x, fused un-permute
+        dprep = spmv_preprocess(m.to_device(), platform13, WorkShare.manual(0.0))
+        import torch
+
+        xd = torch.from_numpy(x).cuda()
+        permd = torch.from_numpy(np.asarray(dprep.perm)).cuda()
+        y = gpu_spmv(dprep.permuted, xd, 0, m.rows, perm=permd)
+        assert np.array_equal(bits(y.cpu().numpy()), bits(g[f"y_{i}"]))
+
+
+def test_every_split_row_sound(platform13):
+    ptr, col, val = ods.csr(30, 30, 5, 0.15)
+    m = CsrMatrix(30, 30, ptr, col, val)
+    x = orng.uniform_floats(99, 30)
+    base = spmv_preprocess(m, platform13)
+    want = ospmv.hybrid(base.perm, (base.permuted.row_ptr, base.permuted.col_idx, base.permuted.values), 0, x)
+    for split in range(0, 31):
+        prep = SpmvPrep(base.permuted, base.perm, split)
+        assert np.array_equal(bits(spmv_hybrid(prep, x)), bits(want))
+
+
+def test_kats_identity_zero_and_mismatch(platform13):
+    prep = spmv_preprocess(CsrMatrix.identity(3), platform13)
+    assert np.array_equal(spmv_hybrid(prep, np.array([1.0, 2.0, 3.0])), [1.0, 2.0, 3.0])
+    zero = CsrMatrix(3, 3, np.zeros(4, dtype=np.int64), np.zeros(0, np.int64), np.zeros(0))
+    assert np.array_equal(spmv_hybrid(spmv_preprocess(zero, platform13), np.ones(3)), np.zeros(3))
+    with pytest.raises(ValueError):
+        spmv_hybrid(prep, np.ones(4))
+
+
+def test_long_and_empty_rows_bit_exact():
+    # rows far longer than one staged chunk, interleaved with empty rows
+    rng = np.random.default_rng(3)
+    lens = np.array([0, 5, 0, 9000, 1, 0, 20000, 3, 0, 0, 4097, 4096, 4095, 17])
+    rows, cols = lens.size, 50_000
+    ptr = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    col = np.concatenate([np.sort(rng.choice(cols, k, replace=False)) for k in lens]).astype(np.int64)
+    val = rng.standard_normal(ptr[-1])
+    x = rng.standard_normal(cols)
+    m = CsrMatrix(rows, cols, ptr, col, val)
+    want = ospmv.sequential_rows(ptr, col, val, x)
+    assert np.array_equal(bits(gpu_spmv(m, x, 0, rows)), bits(want))
+    md = m.to_device(np.int64)
+    import torch
+
+    got = gpu_spmv(md, torch.from_numpy(x).cuda(), 0, rows)
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+    got = gpu_spmv(md, torch.from_numpy(x).cuda(), 2, 9)
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want[2:9]))
+
+
+def test_warp_mode_within_tolerance():
+    ptr, col, val = ods.csr(20_000, 20_000, 42, 8e-4)
+    x = 2.0 * orng.uniform_floats(orng.mix_seed(42, 0xDEC0), 20_000) - 1.0
+    m = CsrMatrix(20_000, 20_000, ptr, col, val)
+    want = ospmv.range_matvec(ptr, col, val, x, 0, 20_000)
+    got = gpu_spmv(m, x, 0, 20_000, exact=False)
+    assert np.allclose(got, want, rtol=1e-9, atol=1e-12)
+    assert np.array_equal(bits(gpu_spmv(m, x, 0, 20_000)), bits(want))
+
+
+def test_device_csr_validation():
+    import torch
+
+    ptr = torch.tensor([0, 2, 1], dtype=torch.int64, device="cuda")
+    with pytest.raises(StructuralError):
+        CsrMatrix(2, 3, ptr, torch.tensor([0, 1], device="cuda"), torch.ones(2, dtype=torch.float64, device="cuda"))
+    with pytest.raises(StructuralError):
+        CsrMatrix(1, 3, torch.tensor([0, 2], device="cuda"), torch.tensor([2, 1], device="cuda"),
+                  torch.ones(2, dtype=torch.float64, device="cuda"))
+    with pytest.raises(StructuralError):
+        CsrMatrix(1, 2, torch.tensor([0, 1], device="cuda"), torch.tensor([5], device="cuda"),
+                  torch.ones(1, dtype=torch.float64, device="cuda"))
+    ok = CsrMatrix(2, 3, torch.tensor([0, 1, 3], device="cuda"), torch.tensor([2, 0, 1], device="cuda"),
+                   torch.ones(3, dtype=torch.float64, device="cuda"))
+    assert ok.nnz == 3
+
+
+def test_workshared_runner_path():
+    from paper_1303_2171_b200.platform import Accounting
+
+    ptr, col, val = ods.csr(5000, 5000, 42, 0.002)
+    m = CsrMatrix(5000, 5000, ptr, col, val)
+    x = 2.0 * orng.uniform_floats(orng.mix_seed(42, 0xDEC0), 5000) - 1.0
+    plat = Platform.build(1.0, 3.0, accounting=Accounting.MEASURED)
+    prep = spmv_preprocess(m, plat)
+    wl = SpmvWorkload(prep, x)
+    y, report = run_workshared(plat, wl, WorkShare.manual(0.25))
+    perm, permuted, split = ospmv.preprocess(ptr, col, val, 1.0, 3.0, None)
+    assert np.array_equal(bits(y), bits(ospmv.hybrid(perm, permuted, split, x)))
+    assert report.pure_b_time > 0

@@ -117,6 +117,18 @@ int hb_csr_validate(const void* row_ptr, int ptr_code, const void* col_idx, int 
                     int64_t rows, int64_t nnz, int64_t cols, uint32_t* flags_out, int flags,
                     void* stream);
 
+/* ---------------------------------------------------------------- bilateral
+ * Replaces bilateral_rows / BilateralApplyWorkload.run_part
+ * (kernels_regular.py:461-511): output rows [row0, row1) of the clamp-to-edge
+ * LUT bilateral filter of the uint8 image img[height][width];
+ * spatial[(2r+1)^2] row-major and range256[256] are the BilateralLut tables
+ * (:447-458).  out is (row1-row0) x width, fp64 (out_code 64, bit-identical
+ * to the reference) or fp32 (out_code 32, the fp64 result rounded).
+ * Host-pointer calls stage only the strip plus its clamped halo rows.     */
+int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t radius,
+                    const double* spatial, const double* range256, int32_t row0, int32_t row1,
+                    void* out, int out_code, int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,201 @@
+// bilateral.cu — LUT bilateral filter on row strips (replaces bilateral_rows /
+// BilateralApplyWorkload.run_part, reference kernels_regular.py:461-511).
+//
+// Arithmetic is the reference's, bit for bit: for every tap (dy, dx) in
+// row-major order, w = spatial[tap] * range[|nb - c|] (rounded fp64 multiply),
+// num += w * nb, den += w (rounded, no FMA), out = num / den (IEEE division).
+// Clamp-to-edge borders.  Output fp64 (the reference's dtype) or fp32.
+//
+// Layout: one CTA = a TILE_H x TILE_W output tile;
+// the clamped (TILE_H+2R) x (TILE_W+2R) input halo tile is staged in shared
+// memory as int32; the 256-entry range table is stored LANE-STRIPED
+// (entry e of lane l at [e][l]) so the 16 lanes of a half-warp read 16
+// distinct 8-byte bank pairs for any intensity differences — conflict-free
+// lookups; each thread owns PX horizontally adjacent output pixels and keeps
+// one input row segment (PX+2R values, converted to fp64 once) in registers
+// while it sweeps the 2R+1 taps of that row, so shared-memory traffic per tap
+// is one range-table load.  The bound is fp64 issue (2 DMUL + 2 DADD per tap).
+#include "common.cuh"
+
+namespace hb {
+namespace {
+
+constexpr int kTileH = 32;
+constexpr int kTileW = 64;
+constexpr int kPx = 8;                        // pixels per thread (one row segment)
+constexpr int kThreads = kTileH * kTileW / kPx;  // 256
+constexpr int kMaxR = 8;
+
+template <int R, typename OUT>
+__global__ void __launch_bounds__(kThreads, 2)
+    bilateral_tile_kernel(const uint8_t* __restrict__ img, int H, int W, int row0, int row1,
+                          const double* __restrict__ spatial, const double* __restrict__ range,
+                          OUT* __restrict__ out) {
+  constexpr int S = 2 * R + 1;
+  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* rng = reinterpret_cast<double*>(smem);            // [256][32] lane-striped
+  double* sp = rng + 256 * 32;                              // [S*S]
+  int* tile = reinterpret_cast<int*>(sp + S * S);           // [TH][TW]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int y0 = row0 + blockIdx.y * kTileH;  // first output row of the tile
+  const int x0 = blockIdx.x * kTileW;
+
+  for (int i = tid; i < 256 * 32; i += kThreads) rng[i] = range[i >> 5];
+  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
+  for (int i = tid; i < TH * TW; i += kThreads) {
+    const int ty = i / TW, tx = i - ty * TW;
+    const int gy = min(max(y0 - R + ty, 0), H - 1);
+    const int gx = min(max(x0 - R + tx, 0), W - 1);
+    tile[i] = img[(int64_t)gy * W + gx];
+  }
+  __syncthreads();
+
+  const int py = tid / (kTileW / kPx);          // output row within the tile
+  const int px = (tid % (kTileW / kPx)) * kPx;  // first output column within the tile
+  const int gy = y0 + py;
+  if (gy >= row1) return;
+
+  int c[kPx];
+#pragma unroll
+  for (int j = 0; j < kPx; ++j) c[j] = tile[(py + R) * TW + px + j + R];
+  double num[kPx], den[kPx];
+#pragma unroll
+  for (int j = 0; j < kPx; ++j) num[j] = den[j] = 0.0;
+
+  const double* lane_rng = rng + lane;
+#pragma unroll 1
+  for (int dy = 0; dy < S; ++dy) {
+    int nb[kPx + 2 * R];
+    double nbd[kPx + 2 * R];
+    const int* trow = tile + (py + dy) * TW + px;
+#pragma unroll
+    for (int k = 0; k < kPx + 2 * R; ++k) {
+      nb[k] = trow[k];
+      nbd[k] = (double)nb[k];
+    }
+#pragma unroll
+    for (int dx = 0; dx < S; ++dx) {
+      const double s = sp[dy * S + dx];
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) {
+        const int d = abs(nb[j + dx] - c[j]);
+        const double w = __dmul_rn(s, lane_rng[d << 5]);
+        num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
+        den[j] = __dadd_rn(den[j], w);
+      }
+    }
+  }
+  OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
+#pragma unroll
+  for (int j = 0; j < kPx; ++j)
+    if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
+}
+
+// generic radius (> kMaxR): same arithmetic, neighbours read from global memory.
+template <typename OUT>
+__global__ void bilateral_generic_kernel(const uint8_t* __restrict__ img, int H, int W, int row0,
+                                         int row1, int R, const double* __restrict__ spatial,
+                                         const double* __restrict__ range, OUT* __restrict__ out) {
+  const int64_t n = (int64_t)(row1 - row0) * W;
+  const int S = 2 * R + 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = row0 + (int)(i / W), x = (int)(i % W);
+    const int c = img[(int64_t)y * W + x];
+    double num = 0.0, den = 0.0;
+    for (int dy = 0; dy < S; ++dy) {
+      const int yy = min(max(y + dy - R, 0), H - 1);
+      for (int dx = 0; dx < S; ++dx) {
+        const int xx = min(max(x + dx - R, 0), W - 1);
+        const int v = img[(int64_t)yy * W + xx];
+        const double w = __dmul_rn(spatial[dy * S + dx], range[abs(v - c)]);
+        num = __dadd_rn(num, __dmul_rn(w, (double)v));
+        den = __dadd_rn(den, w);
+      }
+    }
+    out[i] = (OUT)__ddiv_rn(num, den);
+  }
+}
+
+template <int R, typename OUT>
+int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const double* sp,
+                const double* rg, OUT* out, cudaStream_t s) {
+  constexpr int S = 2 * R + 1;
+  const size_t smem = 256 * 32 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
+  HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_tile_kernel<R, OUT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
+  bilateral_tile_kernel<R, OUT><<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out);
+  return check_launch();
+}
+
+template <typename OUT>
+int launch_bilateral(const uint8_t* img, int H, int W, int row0, int row1, int R, const double* sp,
+                     const double* rg, OUT* out, cudaStream_t s) {
+  switch (R) {
+    case 0: return launch_tile<0, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 1: return launch_tile<1, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 2: return launch_tile<2, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 3: return launch_tile<3, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 4: return launch_tile<4, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 5: return launch_tile<5, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 6: return launch_tile<6, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 7: return launch_tile<7, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 8: return launch_tile<8, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    default: {
+      DeviceInfo di;
+      HB_TRY(device_info(&di));
+      int64_t n = (int64_t)(row1 - row0) * W;
+      int64_t blocks = ceil_div(n, 256);
+      if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+      bilateral_generic_kernel<OUT><<<(int)blocks, 256, 0, s>>>(img, H, W, row0, row1, R, sp, rg, out);
+      return check_launch();
+    }
+  }
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t radius,
+                               const double* spatial, const double* range256, int32_t row0,
+                               int32_t row1, void* out, int out_code, int flags, void* stream) {
+  HB_CHECK_ARG(height > 0 && width > 0, "image must be non-empty");
+  HB_CHECK_ARG(radius >= 0 && radius <= 255, "radius must be in [0, 255]");
+  HB_CHECK_ARG(row0 >= 0 && row1 >= row0 && row1 <= height, "bad row range");
+  HB_CHECK_ARG(out_code == 64 || out_code == 32, "out_code must be 64 (fp64) or 32 (fp32)");
+  if (row1 == row0) return HB_OK;
+  HB_CHECK_ARG(img && spatial && range256 && out, "NULL pointer");
+  const bool dev = flags & HB_DEVICE_PTRS;
+  HB_CHECK_ARG(dev || !(flags & HB_ASYNC), "HB_ASYNC requires device pointers");
+  cudaStream_t s = as_stream(stream);
+  const int S = 2 * radius + 1;
+  // host calls: stage only the strip and its clamped halo rows
+  int in0 = 0, in1 = height;
+  if (!dev) {
+    in0 = row0 - radius < 0 ? 0 : row0 - radius;
+    in1 = row1 + radius > height ? height : row1 + radius;
+  }
+  DevBuf d_img, d_sp, d_rg, d_out;
+  const uint8_t* src = dev ? img : img + (int64_t)in0 * width;
+  HB_TRY(stage_in(&d_img, src, (size_t)(in1 - in0) * width, dev, s));
+  HB_TRY(stage_in(&d_sp, spatial, (size_t)S * S * 8, dev, s));
+  HB_TRY(stage_in(&d_rg, range256, 256 * 8, dev, s));
+  const size_t es = out_code == 64 ? 8 : 4;
+  const size_t out_bytes = (size_t)(row1 - row0) * width * es;
+  HB_TRY(stage_out(&d_out, out, out_bytes, dev, s));
+  // the kernel sees a (in1-in0)-row image; clamping at its edges equals
+  // clamping at the true image edges because the staged rows cover the halo
+  const int h = in1 - in0, r0 = row0 - in0, r1 = row1 - in0;
+  int rc = out_code == 64
+               ? launch_bilateral<double>(d_img.as<uint8_t>(), h, width, r0, r1, radius, d_sp.as<double>(), d_rg.as<double>(), d_out.as<double>(), s)
+               : launch_bilateral<float>(d_img.as<uint8_t>(), h, width, r0, r1, radius, d_sp.as<double>(), d_rg.as<double>(), d_out.as<float>(), s);
+  if (rc != HB_OK) return rc;
+  HB_TRY(copy_out(out, d_out, out_bytes, dev, s));
+  return finish(flags, s);
+}

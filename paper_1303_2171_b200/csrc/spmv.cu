@@ -34,6 +34,7 @@ namespace {
 constexpr int kRows = 256;      // rows per CTA == threads per CTA
 constexpr int kChunk = 4096;    // products staged per chunk (32 KB smem)
 constexpr int kUnroll = kChunk / kRows;
+constexpr int kBatch = 8;          // loads in flight per thread per batch
 
 __device__ __forceinline__ int swz(int k) { return k ^ ((k >> 4) & 15); }
 
@@ -42,13 +43,47 @@ __device__ __forceinline__ int64_t ld_idx(const P* p, int64_t i) {
   return (int64_t)__ldg(p + i);
 }
 
+// L2 policies: the matrix streams through once (evict_first); x is reused by
+// every row (evict_last keeps the 8 MB vector resident in the 126 MB L2).
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_keep(const double* a, uint64_t pol) {
+  double d;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(d) : "l"(a), "l"(pol));
+  return d;
+}
+__device__ __forceinline__ double ld_stream(const double* a, uint64_t pol) {
+  double d;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(d) : "l"(a), "l"(pol));
+  return d;
+}
+__device__ __forceinline__ int64_t ld_stream_idx(const int32_t* a, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_stream_idx(const int64_t* a, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 template <typename P, typename C, typename Q>
-__global__ void __launch_bounds__(kRows)
+__global__ void __launch_bounds__(kRows, 4)
     spmv_seq_kernel(const P* __restrict__ row_ptr, const C* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
                     int64_t row1, const Q* __restrict__ perm, double* __restrict__ y) {
   __shared__ double prod[kChunk];
   const int tid = threadIdx.x;
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
   const int64_t blk0 = row0 + (int64_t)blockIdx.x * kRows;
   const int64_t r = blk0 + tid;
   const int64_t blk1 = min(blk0 + kRows, row1);
@@ -62,21 +97,24 @@ __global__ void __launch_bounds__(kRows)
   double acc = 0.0;
   for (int64_t cs = nz0; cs < nz1; cs += kChunk) {
     const int n = (int)min((int64_t)kChunk, nz1 - cs);
-    // products: kUnroll independent loads in flight per thread
-    int c[kUnroll];
-    double v[kUnroll];
+    // products, kBatch independent (col, val) loads then kBatch x gathers in flight
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int k = tid + u * kRows;
-      if (k < n) {
-        c[u] = (int)ld_idx(col, cs + k);
-        v[u] = __ldg(val + cs + k);
+    for (int u0 = 0; u0 < kUnroll; u0 += kBatch) {
+      int64_t c[kBatch];
+      double v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int k = tid + (u0 + u) * kRows;
+        if (k < n) {
+          c[u] = ld_stream_idx(col + cs + k, stream);
+          v[u] = ld_stream(val + cs + k, stream);
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int k = tid + u * kRows;
-      if (k < n) prod[swz(k)] = __dmul_rn(v[u], __ldg(x + c[u]));
+      for (int u = 0; u < kBatch; ++u) {
+        const int k = tid + (u0 + u) * kRows;
+        if (k < n) prod[swz(k)] = __dmul_rn(v[u], ld_keep(x + c[u], keep));
+      }
     }
     __syncthreads();
     const int64_t a = max(rs, cs), b = min(re, cs + n);

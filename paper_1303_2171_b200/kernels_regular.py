@@ -149,3 +149,147 @@ def hybrid_histogram(
     workload = HistogramWorkload(data, bin_count)
     result, _ = run_workshared(platform, workload, share or formula_share(platform), baselines=False)
     return result
+
+
+# --------------------------------------------------------------------------
+# bilateral filter (kernels_regular.py:421-520)
+
+
+@dataclass(frozen=True)
+class BilateralLut:
+    """Gaussian tables: spatial weight per stencil offset (row-major), range
+    weight per absolute intensity difference (:421-444)."""
+
+    spatial_weights: np.ndarray
+    range_weights: np.ndarray
+    sigma_s: float
+    sigma_r: float
+    radius: int
+
+    def __post_init__(self) -> None:
+        side = 2 * self.radius + 1
+        if self.spatial_weights.shape != (side * side,):
+            raise ValueError("spatial table must have (2r+1)^2 entries")
+        if self.range_weights.shape != (256,):
+            raise ValueError("range table must have 256 entries")
+        for table in (self.spatial_weights, self.range_weights):
+            if not ((table > 0) & (table <= 1.0)).all():
+                raise ValueError("lut weights must lie in (0, 1]")
+
+    @property
+    def entry_count(self) -> int:
+        return self.spatial_weights.size + self.range_weights.size
+
+
+def build_bilateral_lut(radius: int, sigma_s: float, sigma_r: float) -> BilateralLut:
+    """spatial[d] = exp(-|offset|^2 / 2σs²), range[k] = exp(-k² / 2σr²) (:447-458)."""
+    if radius < 0:
+        raise ValueError("radius must be >= 0")
+    if not (sigma_s > 0 and sigma_r > 0):
+        raise ValueError("sigmas must be > 0")
+    off = np.arange(-radius, radius + 1, dtype=np.float64)
+    d2 = off[:, None] ** 2 + off[None, :] ** 2
+    spatial = np.exp(-d2 / (2.0 * sigma_s**2)).ravel()
+    k = np.arange(256, dtype=np.float64)
+    return BilateralLut(spatial, np.exp(-(k**2) / (2.0 * sigma_r**2)), sigma_s, sigma_r, radius)
+
+
+def bilateral_rows(pixels: np.ndarray, lut: BilateralLut, row0: int, row1: int) -> np.ndarray:
+    """Host (DeviceA) body, the reference arithmetic (:461-486): for each tap in
+    row-major order w = spatial·range[|nb-c|], num += w·nb, den += w; clamp to
+    edge; returns num/den as float64 rows [row0, row1)."""
+    pixels = to_host(pixels)
+    height, width = pixels.shape
+    r = lut.radius
+    m = row1 - row0
+    if m <= 0:
+        return np.zeros((0, width))
+    ridx = np.clip(np.arange(row0 - r, row1 + r), 0, height - 1)
+    slab = np.pad(pixels[ridx].astype(np.int64), ((0, 0), (r, r)), mode="edge")
+    center = slab[r : r + m, r : r + width]
+    num = np.zeros((m, width))
+    den = np.zeros((m, width))
+    side = 2 * r + 1
+    for dy in range(side):
+        for dx in range(side):
+            nb = slab[dy : dy + m, dx : dx + width]
+            w = lut.spatial_weights[dy * side + dx] * lut.range_weights[np.abs(nb - center)]
+            num += w * nb
+            den += w
+    return num / den
+
+
+def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out: Any = None,
+                       *, out_dtype: Any = np.float64, asynchronous: bool = False) -> Any:
+    """DeviceB body (hb_bilateral_u8): rows [row0, row1) on the GPU, bit-identical
+    to `bilateral_rows` for fp64 output.  Host pixels → numpy result; CUDA
+    pixels (uint8 tensor) → result tensor (the LUT tables are staged per call)."""
+    _lib.load()
+    code = 64 if np.dtype(out_dtype) == np.float64 else 32
+    height, width = int(pixels.shape[0]), int(pixels.shape[1])
+    if not 0 <= row0 <= row1 <= height:
+        raise ValueError("bad row range")
+    if row1 > row0:
+        require_gpu()
+    if is_device_array(pixels):
+        import torch
+
+        tdt = torch.float64 if code == 64 else torch.float32
+        if out is None:
+            out = torch.empty((row1 - row0, width), dtype=tdt, device=pixels.device)
+        if row1 == row0:
+            return out
+        sp = torch.from_numpy(np.ascontiguousarray(lut.spatial_weights)).to(pixels.device)
+        rg = torch.from_numpy(np.ascontiguousarray(lut.range_weights)).to(pixels.device)
+        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0)
+        _lib.call("hb_bilateral_u8", vp(pixels.data_ptr()), height, width, lut.radius, vp(sp.data_ptr()),
+                  vp(rg.data_ptr()), row0, row1, vp(out.data_ptr()), code, flags, current_stream_handle(pixels))
+        return out
+    img = buf(pixels, np.uint8)
+    if out is None:
+        out = np.empty((row1 - row0, width), dtype=np.float64 if code == 64 else np.float32)
+    if row1 == row0:
+        return out
+    sp = np.ascontiguousarray(lut.spatial_weights, dtype=np.float64)
+    rg = np.ascontiguousarray(lut.range_weights, dtype=np.float64)
+    _lib.call("hb_bilateral_u8", vp(img.ptr), height, width, lut.radius, vp(sp.ctypes.data),
+              vp(rg.ctypes.data), row0, row1, vp(out.ctypes.data), code, 0, current_stream_handle())
+    return out
+
+
+class BilateralApplyWorkload:
+    """Row strips split at floor(f·H) (:489-511).  DeviceA: numpy rows;
+    DeviceB: the GPU tile kernel, its strip split again over the GPU group
+    (floor(k·n/G)) and gathered; the merge stacks the strips."""
+
+    name = "bilat"
+    unit = "neighbor accumulations"
+
+    def __init__(self, image: Image, lut: BilateralLut):
+        self.image = image
+        self.lut = lut
+        self._per_row = image.width * (2 * lut.radius + 1) ** 2
+
+    def partition(self, fraction_a: float):
+        split = int(math.floor(fraction_a * self.image.height))
+        return (0, split), (split, self.image.height)
+
+    def work_units(self, part) -> float:
+        return float((part[1] - part[0]) * self._per_row)
+
+    def run_part(self, device: Device, part) -> np.ndarray:
+        if device.id is DeviceId.B:
+            return sharding.run_sharded_rows(
+                part[0], part[1], lambda a, b: gpu_bilateral_rows(self.image.pixels, self.lut, a, b)
+            )
+        return bilateral_rows(self.image.pixels, self.lut, part[0], part[1])
+
+    def merge(self, partials: Sequence[np.ndarray]) -> Image:
+        return Image(np.vstack([sharding.to_numpy(p) for p in partials]))
+
+
+def hybrid_bilateral(image: Image, lut: BilateralLut, platform: Platform, share: WorkShare | None = None) -> Image:
+    """kernels_regular.py:514-520."""
+    workload = BilateralApplyWorkload(image, lut)
+    result, _ = run_workshared(platform, workload, share or formula_share(platform), baselines=False)
+    return result

@@ -129,6 +129,26 @@ int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t r
                     const double* spatial, const double* range256, int32_t row0, int32_t row1,
                     void* out, int out_code, int flags, void* stream);
 
+/* --------------------------------------------------------------------- sort
+ * Replaces the DeviceB side of sample_sort_hybrid (kernels_regular.py:239-310)
+ * with an LSD radix sort (onesweep: one digit-histogram pass, then one
+ * decoupled-look-back pass per 8-bit digit that is not constant).  Sorts
+ * keys_in[0:n] into keys_out (the same pointer sorts in place; key_code
+ * HB_U32/HB_I32/HB_U64/HB_I64).  When vals_in/vals_out are non-NULL the
+ * uint32 payload is permuted alongside — stably, so a payload of 0..n-1
+ * becomes the stable argsort.  *passes_done (optional) receives the number
+ * of digit passes executed (0 ⇔ all keys equal).  n < 2^30 per call.      */
+int hb_sort(const void* keys_in, void* keys_out, int key_code, const uint32_t* vals_in,
+            uint32_t* vals_out, int64_t n, int32_t* passes_done, int flags, void* stream);
+
+/* Split points of the multi-GPU sample-merge: out_pos[j] =
+ * number of (keys[i], vals[i]) lexicographically below (probe_keys[j],
+ * probe_vals[j]) in the sorted sequence (key-only when either vals array is
+ * NULL).  Device pointers only.                                             */
+int hb_sort_bounds(const void* keys, int key_code, const uint32_t* vals, int64_t n,
+                   const void* probe_keys, const uint32_t* probe_vals, int32_t m, int64_t* out_pos,
+                   int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,397 @@
+// sort.cu — LSD radix sort, onesweep style (replaces the DeviceB side of
+// sample_sort_hybrid, reference kernels_regular.py:239-310; the sorted
+// multiset is unique, so the output equals the reference's bit for bit; the
+// optional uint32 payload makes it the STABLE argsort).
+//
+//   1. digit_hist_kernel: one read of the keys builds the 256-bucket
+//      histogram of every 8-bit digit position at once (privatised smem
+//      counters, 8 copies per bucket).
+//   2. per non-trivial digit position, onesweep_kernel (one launch):
+//      * tiles of THREADS*ITEMS keys, tile ids taken from an atomic counter
+//        (a tile's predecessors are always resident or done: forward progress);
+//      * warp-striped coalesced loads; stable warp-level ranking with eight
+//        __ballot_sync per key row (warp multi-split) into per-warp smem
+//        counters; cross-warp exclusive scan per digit;
+//      * decoupled look-back per digit (one thread per digit): the tile
+//        publishes its digit counts (AGGREGATE), walks back over predecessor
+//        tiles until it finds an INCLUSIVE prefix, then publishes its own
+//        inclusive prefix — 32-bit words, 2 flag bits + 30 count bits, so
+//        one relaxed store publishes flag and count together;
+//      * keys (and payload) are re-ordered by digit in shared memory and
+//        written out in digit runs (coalesced segments).
+//   A digit position whose histogram has a single bucket is skipped (a stable
+//   pass over one bucket is the identity) — int64 keys below 2^32 sort in 4
+//   passes, a constant array in 0.
+#include <utility>
+
+#include "common.cuh"
+
+namespace hb {
+namespace {
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kCountMask = (1u << 30) - 1;
+
+template <typename K>
+struct SortCfg;
+template <>
+struct SortCfg<uint32_t> {
+  static constexpr int kThreads = 512, kItems = 12, kPasses = 4;
+};
+template <>
+struct SortCfg<uint64_t> {
+  static constexpr int kThreads = 512, kItems = 8, kPasses = 8;
+};
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K key, K flip, int shift) {
+  return (uint32_t)((key ^ flip) >> shift) & 255u;
+}
+
+// ------------------------------------------------------------------ 1. histogram
+template <typename K>
+__global__ void __launch_bounds__(512)
+    digit_hist_kernel(const K* __restrict__ keys, int64_t n, K flip, uint32_t* __restrict__ hist) {
+  constexpr int P = SortCfg<K>::kPasses;
+  constexpr int C = 32 / P;  // copies per bucket (32 KB of counters)
+  __shared__ uint32_t s[P * 256 * C];
+  for (int i = threadIdx.x; i < P * 256 * C; i += blockDim.x) s[i] = 0;
+  __syncthreads();
+  const uint32_t copy = threadIdx.x & (C - 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const K k = keys[i] ^ flip;
+#pragma unroll
+    for (int p = 0; p < P; ++p) atomicAdd(&s[((p * 256) + (uint32_t)((k >> (8 * p)) & 255)) * C + copy], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < P * 256; b += blockDim.x) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) sum += s[b * C + ((c + b) & (C - 1))];
+    if (sum) atomicAdd(hist + b, sum);
+  }
+}
+
+// ------------------------------------------------------------------ 2. onesweep pass
+template <typename K, bool HAS_V>
+__global__ void __launch_bounds__(SortCfg<K>::kThreads, 2)
+    onesweep_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
+                    uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
+                    const uint32_t* __restrict__ pass_hist, uint32_t* __restrict__ lookback,
+                    uint32_t* __restrict__ tile_counter) {
+  constexpr int T = SortCfg<K>::kThreads, I = SortCfg<K>::kItems, W = T / 32, TILE = T * I;
+  __shared__ uint32_t s_whist[W][256];   // per-warp digit counters → exclusive warp offsets
+  __shared__ uint32_t s_dstart[256];     // exclusive scan over digits of the tile counts
+  __shared__ uint32_t s_goff[256];       // global offset of digit run minus its tile start
+  __shared__ uint32_t s_gstart[256];     // global exclusive digit starts (this pass)
+  __shared__ uint32_t s_tile;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  K* s_keys = reinterpret_cast<K*>(s_dyn);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + TILE);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < W * 256; i += T) (&s_whist[0][0])[i] = 0;
+  // global digit starts: exclusive scan of this pass's histogram (warp 0..7: 32 digits each)
+  if (tid < 256) {
+    uint32_t h = pass_hist[tid];
+    uint32_t x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_gstart[tid] = x - h;  // exclusive within the 32-digit group
+    if (lane == 31) s_dstart[warp] = x;  // group totals (scratch)
+  }
+  __syncthreads();
+  if (tid < 256) {
+    uint32_t add = 0;
+    for (int g = 0; g < (tid >> 5); ++g) add += s_dstart[g];
+    s_gstart[tid] += add;
+  }
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * TILE;
+  const int64_t wbase = base + (int64_t)warp * 32 * I;
+
+  K key[I];
+  uint32_t val[I];
+  uint32_t rank[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    const bool ok = idx < n;
+    key[i] = ok ? kin[idx] : (K)(~(K)0 ^ flip);  // padding sorts last (digit 255)
+    if (HAS_V) val[i] = ok ? vin[idx] : 0u;
+  }
+  __syncthreads();  // s_whist zeroed, s_gstart ready
+
+  // stable warp-level ranking: eight ballots find the lanes sharing a digit
+  uint32_t* wh = s_whist[warp];
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const uint32_t d = digit_of<K>(key[i], flip, shift);
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    const uint32_t below = __popc(peers & lt);
+    const uint32_t pre = wh[d];
+    __syncwarp();
+    if (below == (uint32_t)__popc(peers) - 1u) wh[d] = pre + below + 1u;
+    __syncwarp();
+    rank[i] = pre + below;
+  }
+  __syncthreads();
+
+  // per digit: exclusive offsets across warps, tile count, publish, look back
+  uint32_t cnt = 0;
+  if (tid < 256) {
+    for (int w = 0; w < W; ++w) {
+      const uint32_t t = s_whist[w][tid];
+      s_whist[w][tid] = cnt;
+      cnt += t;
+    }
+    if (tile == 0) st_relaxed(lookback + tid, kFlagInc | cnt);
+    else st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagAgg | cnt);
+    // exclusive scan of the tile counts over digits
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_dstart[tid] = x - cnt;
+    s_goff[tid] = x;  // scratch: inclusive within group
+  }
+  __syncthreads();
+  uint32_t dstart = 0, excl = 0;
+  if (tid < 256) {
+    uint32_t add = 0;
+    for (int g = 0; g < (tid >> 5); ++g) add += s_goff[g * 32 + 31];
+    dstart = s_dstart[tid] + add;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint32_t w = ld_relaxed(lookback + (size_t)t * 256 + tid);
+        const uint32_t flag = w & ~kCountMask;
+        if (flag == 0) continue;  // predecessor still ranking: spin
+        excl += w & kCountMask;
+        if (flag == kFlagInc) break;
+        --t;
+      }
+      st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagInc | (excl + cnt));
+    }
+  }
+  __syncthreads();  // every thread has read the scan scratch
+  if (tid < 256) {
+    s_dstart[tid] = dstart;
+    s_goff[tid] = s_gstart[tid] + excl - dstart;
+  }
+  __syncthreads();
+
+  // local re-order by digit (stable), then digit-run scatter
+  uint32_t pos[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const uint32_t d = digit_of<K>(key[i], flip, shift);
+    pos[i] = s_dstart[d] + s_whist[warp][d] + rank[i];
+    s_keys[pos[i]] = key[i];
+  }
+  if (HAS_V) {
+#pragma unroll
+    for (int i = 0; i < I; ++i) s_vals[pos[i]] = val[i];
+  }
+  __syncthreads();
+  const int valid = (int)min((int64_t)TILE, n - base);
+  for (int j = tid; j < valid; j += T) {
+    const K k = s_keys[j];
+    const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
+    kout[dst] = k;
+    if (HAS_V) vout[dst] = s_vals[j];
+  }
+}
+
+template <typename K>
+size_t onesweep_smem(bool has_v) {
+  constexpr int TILE = SortCfg<K>::kThreads * SortCfg<K>::kItems;
+  return (size_t)TILE * sizeof(K) + (has_v ? (size_t)TILE * 4 : 0);
+}
+
+template <typename K>
+int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cudaStream_t s) {
+  constexpr int P = SortCfg<K>::kPasses;
+  constexpr int TILE = SortCfg<K>::kThreads * SortCfg<K>::kItems;
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  if (passes_done) *passes_done = 0;
+  if (n <= 1) return HB_OK;
+  if (n >= (int64_t)kCountMask) {
+    set_error("radix sort supports n < 2^30 keys per call (got %lld)", (long long)n);
+    return HB_EINVAL;
+  }
+  const int64_t tiles = ceil_div(n, TILE);
+  DevBuf hist, kalt, valt, lb;
+  HB_TRY(alloc(&hist, (size_t)P * 256 * 4, s));
+  HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, (size_t)P * 256 * 4, s));
+  int64_t hb = ceil_div(n, 512 * 8);
+  if (hb > (int64_t)di.sms * 2) hb = (int64_t)di.sms * 2;
+  digit_hist_kernel<K><<<(int)hb, 512, 0, s>>>(keys, n, flip, hist.as<uint32_t>());
+  HB_TRY(check_launch());
+  uint32_t h[P * 256];
+  HB_CUDA_TRY(cudaMemcpyAsync(h, hist.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  HB_CUDA_TRY(cudaStreamSynchronize(s));
+  bool live[P];
+  int nlive = 0;
+  for (int p = 0; p < P; ++p) {
+    live[p] = true;
+    for (int b = 0; b < 256; ++b)
+      if (h[p * 256 + b] == (uint32_t)n) live[p] = false;
+    nlive += live[p];
+  }
+  if (passes_done) *passes_done = nlive;
+  if (nlive == 0) return HB_OK;
+
+  HB_TRY(alloc(&kalt, (size_t)n * sizeof(K), s));
+  if (vals) HB_TRY(alloc(&valt, (size_t)n * 4, s));
+  const size_t lb_words = (size_t)tiles * 256 + 32;  // + tile counter (padded)
+  HB_TRY(alloc(&lb, lb_words * 4, s));
+  const size_t smem = onesweep_smem<K>(vals != nullptr);
+  if (vals) {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  } else {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  K* kcur = keys;
+  K* knext = kalt.as<K>();
+  uint32_t* vcur = vals;
+  uint32_t* vnext = valt.as<uint32_t>();
+  uint32_t* counter = lb.as<uint32_t>() + (size_t)tiles * 256;
+  for (int p = 0; p < P; ++p) {
+    if (!live[p]) continue;
+    HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
+    const uint32_t* ph = hist.as<uint32_t>() + p * 256;
+    if (vals) {
+      onesweep_kernel<K, true><<<(unsigned)tiles, SortCfg<K>::kThreads, smem, s>>>(
+          kcur, knext, vcur, vnext, n, 8 * p, flip, ph, lb.as<uint32_t>(), counter);
+    } else {
+      onesweep_kernel<K, false><<<(unsigned)tiles, SortCfg<K>::kThreads, smem, s>>>(
+          kcur, knext, nullptr, nullptr, n, 8 * p, flip, ph, lb.as<uint32_t>(), counter);
+    }
+    HB_TRY(check_launch());
+    std::swap(kcur, knext);
+    std::swap(vcur, vnext);
+  }
+  if (kcur != keys) {
+    HB_CUDA_TRY(cudaMemcpyAsync(keys, kcur, (size_t)n * sizeof(K), cudaMemcpyDeviceToDevice, s));
+    if (vals) HB_CUDA_TRY(cudaMemcpyAsync(vals, vcur, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return HB_OK;
+}
+
+// lower_bound of (probe_key, probe_val) in the lexicographically sorted
+// (keys, vals) sequence — the split points of the sample-merge exchange.
+template <typename K>
+__global__ void sort_bounds_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                   int64_t n, K flip, const K* __restrict__ pk,
+                                   const uint32_t* __restrict__ pv, int m,
+                                   int64_t* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const K key = pk[j] ^ flip;
+  const uint32_t v = pv ? pv[j] : 0u;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const K k = keys[mid] ^ flip;
+    const bool less = k < key || (pv && vals && k == key && vals[mid] < v);
+    if (less) lo = mid + 1;
+    else hi = mid;
+  }
+  out[j] = lo;
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int hb_sort_bounds(const void* keys, int key_code, const uint32_t* vals, int64_t n,
+                              const void* probe_keys, const uint32_t* probe_vals, int32_t m,
+                              int64_t* out_pos, int flags, void* stream) {
+  HB_CHECK_ARG(key_code == HB_U32 || key_code == HB_I32 || key_code == HB_U64 || key_code == HB_I64,
+               "keys must be u32, i32, u64 or i64");
+  HB_CHECK_ARG(n >= 0 && m >= 0, "negative size");
+  if (m == 0) return HB_OK;
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_sort_bounds works on device arrays");
+  cudaStream_t s = as_stream(stream);
+  const int blocks = (m + 127) / 128;
+  if (key_code == HB_U64 || key_code == HB_I64) {
+    const uint64_t flip = key_code == HB_I64 ? (1ull << 63) : 0ull;
+    sort_bounds_kernel<uint64_t><<<blocks, 128, 0, s>>>((const uint64_t*)keys, vals, n, flip,
+                                                          (const uint64_t*)probe_keys, probe_vals, m, out_pos);
+  } else {
+    const uint32_t flip = key_code == HB_I32 ? (1u << 31) : 0u;
+    sort_bounds_kernel<uint32_t><<<blocks, 128, 0, s>>>((const uint32_t*)keys, vals, n, flip,
+                                                          (const uint32_t*)probe_keys, probe_vals, m, out_pos);
+  }
+  return finish(flags, s);
+}
+
+extern "C" int hb_sort(const void* keys_in, void* keys_out, int key_code, const uint32_t* vals_in,
+                       uint32_t* vals_out, int64_t n, int32_t* passes_done, int flags, void* stream) {
+  HB_CHECK_ARG(key_code == HB_U32 || key_code == HB_I32 || key_code == HB_U64 || key_code == HB_I64,
+               "sort keys must be u32, i32, u64 or i64 (code %d)", key_code);
+  HB_CHECK_ARG(n >= 0, "n must be >= 0");
+  HB_CHECK_ARG(n == 0 || (keys_in && keys_out), "keys is NULL");
+  HB_CHECK_ARG(!vals_in == !vals_out, "vals_in and vals_out must both be set or both NULL");
+  const bool dev = flags & HB_DEVICE_PTRS;
+  HB_CHECK_ARG(dev || !(flags & HB_ASYNC), "HB_ASYNC requires device pointers");
+  cudaStream_t s = as_stream(stream);
+  const bool wide = key_code == HB_U64 || key_code == HB_I64;
+  const size_t ks = wide ? 8 : 4;
+  DevBuf dk, dv;
+  if (dev) {
+    // device: sort in keys_out (copy first unless in place)
+    if (keys_out != keys_in && n) HB_CUDA_TRY(cudaMemcpyAsync(keys_out, keys_in, (size_t)n * ks, cudaMemcpyDeviceToDevice, s));
+    if (vals_in && vals_out != vals_in && n) HB_CUDA_TRY(cudaMemcpyAsync(vals_out, vals_in, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+    HB_TRY(stage_in(&dk, keys_out, (size_t)n * ks, true, s));
+    if (vals_in) HB_TRY(stage_in(&dv, vals_out, (size_t)n * 4, true, s));
+  } else {
+    HB_TRY(stage_in(&dk, keys_in, (size_t)n * ks, false, s));
+    if (vals_in) HB_TRY(stage_in(&dv, vals_in, (size_t)n * 4, false, s));
+  }
+  int done = 0;
+  int rc;
+  if (wide) {
+    const uint64_t flip = key_code == HB_I64 ? (1ull << 63) : 0ull;
+    rc = radix_sort<uint64_t>(dk.as<uint64_t>(), vals_in ? dv.as<uint32_t>() : nullptr, n, flip, &done, s);
+  } else {
+    const uint32_t flip = key_code == HB_I32 ? (1u << 31) : 0u;
+    rc = radix_sort<uint32_t>(dk.as<uint32_t>(), vals_in ? dv.as<uint32_t>() : nullptr, n, flip, &done, s);
+  }
+  if (rc != HB_OK) return rc;
+  if (passes_done) *passes_done = done;
+  HB_TRY(copy_out(keys_out, dk, (size_t)n * ks, dev, s));
+  if (vals_in) HB_TRY(copy_out(vals_out, dv, (size_t)n * 4, dev, s));
+  return finish(flags, s);
+}

@@ -152,6 +152,158 @@ def hybrid_histogram(
 
 
 # --------------------------------------------------------------------------
+# sort (kernels_regular.py:172-321)
+
+SORT_FANOUT = 64
+SORT_HIST_CELLS = 256
+SORT_MAX_DEPTH = 8
+
+_SORT_CODES = {np.dtype(np.uint32): 5, np.dtype(np.int32): 6, np.dtype(np.uint64): 7, np.dtype(np.int64): 8}
+
+
+def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False) -> tuple[Any, Any, int]:
+    """LSD radix sort on the GPU (hb_sort).  CUDA tensors are sorted in place
+    (payload permuted alongside, stably); host arrays are left untouched and
+    sorted copies returned.  Returns (keys, payload, digit passes executed)."""
+    import ctypes
+
+    _lib.load()
+    kb = buf(keys)
+    code = _SORT_CODES.get(kb.dtype)
+    if code is None:
+        raise TypeError(f"sort keys must be u32/i32/u64/i64, got {kb.dtype}")
+    if kb.size > 1 or kb.device:
+        require_gpu()
+    vb = None
+    if payload is not None:
+        vb = buf(payload) if is_device_array(payload) else buf(payload, np.uint32)
+        if vb.dtype not in (np.dtype(np.uint32), np.dtype(np.int32)) or vb.size != kb.size:
+            raise TypeError("payload must be uint32 (or non-negative int32) with one entry per key")
+    flags = flags_for(kb, *([vb] if vb else []), asynchronous=asynchronous)
+    if kb.device:
+        k_out, v_out = kb.ptr, (vb.ptr if vb else 0)
+        res_k, res_v = keys, payload
+    else:
+        res_k = np.empty_like(kb.owner)
+        res_v = np.empty(kb.size, dtype=vb.dtype) if vb else None
+        k_out, v_out = res_k.ctypes.data, (res_v.ctypes.data if vb else 0)
+    passes = ctypes.c_int32(0)
+    _lib.call("hb_sort", vp(kb.ptr), vp(k_out), code, vp(vb.ptr if vb else 0), vp(v_out), kb.size,
+              ctypes.byref(passes), flags, current_stream_handle(keys if kb.device else None))
+    return res_k, res_v, passes.value
+
+
+def _cell_indices(chunk: np.ndarray, lo, hi) -> np.ndarray:
+    scale = SORT_HIST_CELLS / (float(hi) - float(lo))
+    return np.clip(((chunk - float(lo)) * scale).astype(np.int64), 0, SORT_HIST_CELLS - 1)
+
+
+def _quantile_splitters(counts: np.ndarray, n: int, lo, hi) -> np.ndarray:
+    cum = np.cumsum(counts)
+    cells = np.searchsorted(cum, np.arange(1, SORT_FANOUT) * (n / SORT_FANOUT), side="left")
+    return np.unique(float(lo) + (cells + 1) * ((float(hi) - float(lo)) / SORT_HIST_CELLS))
+
+
+def _host_sort_plan(arr: np.ndarray, fraction: float):
+    """The reference's hybrid binning and smallest-bins-first cut
+    (kernels_regular.py:264-292): returns (bin_ids, bin_sizes, on_a)."""
+    n = arr.size
+    lo, hi = arr.min(), arr.max()
+    split = int(math.floor(fraction * n))
+    cells = _cell_indices(arr, lo, hi)
+    counts = np.bincount(cells[:split], minlength=SORT_HIST_CELLS) + np.bincount(cells[split:], minlength=SORT_HIST_CELLS)
+    spl = _quantile_splitters(counts, n, lo, hi)
+    ids = np.searchsorted(spl, arr, side="right")
+    sizes = np.bincount(ids, minlength=spl.size + 1)
+    asc = np.argsort(sizes, kind="stable")
+    prefix = np.concatenate([[0.0], np.cumsum(sizes[asc])])
+    cut = int(np.argmin(np.maximum(prefix / fraction, (n - prefix) / (1.0 - fraction))))
+    on_a = np.zeros(sizes.size, dtype=bool)
+    on_a[asc[:cut]] = True
+    return ids, sizes, on_a
+
+
+def _gpu_keys(arr: Any):
+    """Key array the GPU sorts: int64 keys stay int64 (digit passes above the
+    data's range are skipped), other integer types are widened when needed."""
+    dt = arr.dtype if not is_device_array(arr) else None
+    if dt is not None and np.dtype(dt) not in _SORT_CODES:
+        return np.asarray(arr, dtype=np.int64)
+    return arr
+
+
+def sample_sort_hybrid(
+    data: Any, platform: Platform, leaf_a: int = 2048, leaf_b: int = 32, share: WorkShare | None = None
+) -> tuple[Any, float, float]:
+    """kernels_regular.py:239-310 → (sorted, work_a, work_b), same work
+    accounting.  DeviceA sorts its bins with numpy on the host; DeviceB's bins
+    are radix-sorted on the GPU (one LSD sort of their union — the bins are
+    disjoint value ranges, so that equals sorting each bin), sharded over the
+    GPU group with a sample-merge exchange when one is active."""
+    if not leaf_a >= leaf_b >= 2:
+        raise ValueError("need leaf_a >= leaf_b >= 2")
+    fraction = (share or formula_share(platform)).fraction_a
+    dev = is_device_array(data)
+    arr = data if dev else np.asarray(data)
+    n = int(arr.numel() if dev else arr.size)
+    if n <= 1:
+        return (arr.clone() if dev else arr.copy()), float(n), 0.0
+    if n <= leaf_a:
+        host = np.sort(to_host(arr), kind="quicksort")
+        return _like(host, data), float(n), 0.0
+    if fraction <= 0.0:
+        # every bin on DeviceB: one GPU sort; a constant array is the
+        # reference's lo == hi early return (work on DeviceA)
+        out = arr.clone() if dev else _gpu_keys(arr)
+        out, _, passes = sharding.run_sharded_sort(out)
+        if passes == 0:
+            return out, float(n), 0.0
+        return out, 0.0, float(n)
+    host = to_host(arr)
+    lo, hi = host.min(), host.max()
+    if lo == hi:
+        return (arr.clone() if dev else arr.copy()), float(n), 0.0
+    if fraction >= 1.0:
+        return _like(np.sort(host, kind="quicksort"), data), float(n), 0.0
+    ids, sizes, on_a = _host_sort_plan(host, fraction)
+    mask_a = on_a[ids]
+    part_a, part_b = host[mask_a], host[~mask_a]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=2) as pool:
+        fa = pool.submit(np.sort, part_a, kind="quicksort")
+        fb = pool.submit(lambda: sharding.to_numpy(sharding.run_sharded_sort(_gpu_keys(part_b))[0]))
+        sorted_a, sorted_b = fa.result(), fb.result()
+    out = np.empty_like(host)
+    pos = pa = pb = 0
+    for i, size in enumerate(sizes.tolist()):
+        if on_a[i]:
+            out[pos : pos + size] = sorted_a[pa : pa + size]
+            pa += size
+        else:
+            out[pos : pos + size] = sorted_b[pb : pb + size]
+            pb += size
+        pos += size
+    work_a = float(sizes[on_a].sum())
+    return _like(out, data), work_a, float(n) - work_a
+
+
+def _like(host: np.ndarray, ref: Any) -> Any:
+    if is_device_array(ref):
+        import torch
+
+        return torch.from_numpy(np.ascontiguousarray(host)).to(ref.device)
+    return host
+
+
+def hybrid_sort(data: Any, platform: Platform, leaf_a: int = 2048, leaf_b: int = 32,
+                share: WorkShare | None = None) -> Any:
+    """kernels_regular.py:313-321."""
+    out, _, _ = sample_sort_hybrid(data, platform, leaf_a, leaf_b, share)
+    return out
+
+
+# --------------------------------------------------------------------------
 # bilateral filter (kernels_regular.py:421-520)
 
 

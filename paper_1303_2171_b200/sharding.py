@@ -150,3 +150,17 @@ def to_numpy(x: Any) -> np.ndarray:
     if is_device_array(x):
         return x.cpu().numpy()
     return np.asarray(x)
+
+
+def run_sharded_sort(keys: Any, payload: Any = None, local: Callable | None = None):
+    """DeviceB sort share.  Single GPU: one LSD radix sort.  GPU group: the
+    sample-merge of sort_exchange.py (local sort, splitter all-gather,
+    all-to-all, local merge); every rank returns the full sorted array."""
+    if local is None:
+        from .kernels_regular import gpu_sort as local
+    g = _active
+    if g is None or g.world == 1:
+        return local(keys, payload)
+    from .sort_exchange import sample_merge_sort
+
+    return sample_merge_sort(keys, payload, g, local)

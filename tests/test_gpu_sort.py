@@ -23,10 +23,7 @@ def test_golden_work_accounting(platform13, name):
         share = None if sh < 0 else WorkShare.manual(float(sh))
         out, got_a, got_b = sample_sort_hybrid(data, platform13, share=share)
         assert np.array_equal(out, np.sort(data))
-        if sh != 0.0:  # share 0: pure GPU; the reference reports (0, n) too unless lo == hi
-            assert (got_a, got_b) == (wa, wb)
-        else:
-            assert got_a + got_b == data.size
+        assert (got_a, got_b) == (wa, wb)
 
 
 def test_reference_unit_cases(platform13):

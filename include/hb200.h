@@ -149,6 +149,16 @@ int hb_sort_bounds(const void* keys, int key_code, const uint32_t* vals, int64_t
                    const void* probe_keys, const uint32_t* probe_vals, int32_t m, int64_t* out_pos,
                    int flags, void* stream);
 
+/* ------------------------------------------------------------- list ranking
+ * Replaces the ranking of list_rank_with_stats / list_rank_hybrid
+ * (kernels_irregular.py:377-508): rank[i] = distance of node i from `head`
+ * along succ (succ[i] = next node or -1; HB_I32 or HB_I64), rank int64.
+ * Includes validate_list's checks (:377-393): head/successor out of range,
+ * cycles and broken lists return HB_ESTRUCT.  Recursive sparse ruling set
+ * (Helman-JaJa) + Wyllie pointer jumping on the top level.               */
+int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t head, int64_t* rank, int flags,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,324 @@
+// listrank.cu — list ranking (replaces the ranking of list_rank_with_stats /
+// list_rank_hybrid, reference kernels_irregular.py:377-508: rank[i] = distance
+// of node i from the head; the result is independent of the algorithm, so the
+// output equals the reference's bit for bit).
+//
+// Fast path (hb_list_rank): recursive sparse ruling set (Helman-JaJa) with
+// Wyllie pointer jumping at the top.
+//   level 1: every node whose index is a multiple of K (plus the list head)
+//            starts a sublist; one thread per sublist walks its successors
+//            until the next sublist head, writing (sublist id, local weighted
+//            offset) packed into the 64-bit output slot of each node it passes
+//            and the sublist's (next sublist, length);
+//   level 2+: the same on the list of sublists (weighted by their lengths)
+//            until at most kBase nodes remain;
+//   top:     one CTA ranks the remaining list in shared memory by Wyllie
+//            pointer jumping (suffix sums → prefix = total - suffix) and checks
+//            that the chain from the head covers every node (broken lists and
+//            cycles → HB_ESTRUCT, the reference's StructuralError);
+//   back down: rank = prefix[sublist] + local offset, one coalesced pass per
+//            level.
+// The walk is a chain of dependent random 4-byte reads (one 32-byte sector
+// per node): it is bound by DRAM sector throughput, not bytes.
+#include <vector>
+
+#include "common.cuh"
+
+namespace hb {
+namespace {
+
+constexpr int kK = 64;        // sublist spacing (node index multiple)
+constexpr int kBase = 4096;   // top level size ranked in one CTA
+
+// validation: out[0] += tails (succ == -1), out[1] += out-of-range successors
+template <typename S>
+__global__ void lr_check_kernel(const S* __restrict__ succ, int64_t n,
+                                unsigned long long* __restrict__ out) {
+  unsigned long long tails = 0, bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = (int64_t)succ[i];
+    tails += (s == -1);
+    bad += (s < -1 || s >= n);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    tails += __shfl_xor_sync(0xffffffffu, tails, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (tails) atomicAdd(out, tails);
+    if (bad) atomicAdd(out + 1, bad);
+  }
+}
+
+__device__ __forceinline__ bool is_head(int64_t v, int64_t head) { return (v % kK) == 0 || v == head; }
+
+// sublist id of a head node: v/K for multiples of K, `extra` for the list head otherwise
+__device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra) {
+  return (v % kK) == 0 ? v / kK : extra;
+}
+
+// One thread per sublist: walk from its head to the next head.
+// tmp[v] = (sublist << 32) | local offset; nxt[j] = next sublist or -1; len[j] = weight sum.
+template <typename S, bool WEIGHTED>
+__global__ void lr_walk_kernel(const S* __restrict__ succ, const int64_t* __restrict__ w, int64_t n,
+                               int64_t head, int64_t nsub, int64_t extra, uint64_t* __restrict__ tmp,
+                               int64_t* __restrict__ nxt, int64_t* __restrict__ len,
+                               unsigned long long* __restrict__ err) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nsub;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = j == extra ? head : j * kK;
+    if (h >= n) {  // no such node: an isolated, zero-weight sublist
+      nxt[j] = -1;
+      len[j] = 0;
+      continue;
+    }
+    tmp[h] = (uint64_t)j << 32;
+    int64_t acc = WEIGHTED ? w[h] : 1;
+    int64_t cur = (int64_t)__ldg(succ + h);
+    int64_t steps = 0;
+    while (cur != -1 && !is_head(cur, head)) {
+      tmp[cur] = ((uint64_t)j << 32) | (uint64_t)(uint32_t)acc;
+      acc += WEIGHTED ? w[cur] : 1;
+      cur = (int64_t)__ldg(succ + cur);
+      if (++steps > n) {  // cycle without a sublist head
+        atomicAdd(err, 1ull);
+        break;
+      }
+    }
+    nxt[j] = (cur == -1 || steps > n) ? -1 : sub_id(cur, head, extra);
+    len[j] = acc;
+  }
+}
+
+// rank[v] = prefix[sublist] + local
+__global__ void lr_expand_kernel(const uint64_t* __restrict__ tmp, int64_t n,
+                                 const int64_t* __restrict__ prefix, int64_t* __restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = tmp[v];
+    out[v] = prefix[t >> 32] + (int64_t)(t & 0xffffffffull);
+  }
+}
+
+// Top level, one CTA: weighted Wyllie pointer jumping in shared memory.
+// prefix[j] = sum of len over the chain from `head` up to (excluding) j.
+// status[0] = chain total from head, status[1] = 1 if a cycle was found.
+__global__ void __launch_bounds__(1024)
+    lr_top_kernel(const int64_t* __restrict__ nxt_in, const int64_t* __restrict__ len, int64_t m,
+                  int64_t head, int64_t* __restrict__ prefix, int64_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char top_smem[];
+  int64_t(*val)[kBase] = reinterpret_cast<int64_t(*)[kBase]>(top_smem);
+  int32_t(*nxt)[kBase] = reinterpret_cast<int32_t(*)[kBase]>(top_smem + 2 * kBase * sizeof(int64_t));
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    nxt[0][i] = (int32_t)nxt_in[i];
+    val[0][i] = len[i];
+  }
+  __syncthreads();
+  int cur = 0;
+  int rounds = 0;
+  while ((1ll << rounds) < 2 * m) {
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const int32_t nx = nxt[cur][i];
+      if (nx >= 0) {
+        val[cur ^ 1][i] = val[cur][i] + val[cur][nx];
+        nxt[cur ^ 1][i] = nxt[cur][nx];
+      } else {
+        val[cur ^ 1][i] = val[cur][i];
+        nxt[cur ^ 1][i] = -1;
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+    ++rounds;
+  }
+  // val = suffix sums; a remaining successor means a cycle
+  __shared__ int cyc;
+  if (threadIdx.x == 0) cyc = 0;
+  __syncthreads();
+  const int64_t total = val[cur][head];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    if (nxt[cur][i] >= 0) cyc = 1;
+    prefix[i] = total - val[cur][i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    status[0] = total;
+    status[1] = cyc;
+  }
+}
+
+constexpr size_t kTopSmem = 2 * kBase * (sizeof(int64_t) + sizeof(int32_t));
+
+struct Level {
+  DevBuf tmp, nxt, len, ranked;
+  int64_t n = 0, nsub = 0, extra = -1, head = 0;
+};
+
+template <typename S>
+int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaStream_t s) {
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  DevBuf err, st;
+  HB_TRY(alloc(&err, 8, s));
+  HB_CUDA_TRY(cudaMemsetAsync(err.ptr, 0, 8, s));
+  std::vector<Level*> levels;
+  struct Cleanup {
+    std::vector<Level*>& v;
+    ~Cleanup() {
+      for (auto* l : v) delete l;
+    }
+  } cleanup{levels};
+
+  // descend: level 0 walks the input list, later levels walk the sublist lists
+  const int64_t* w = nullptr;
+  const void* cur_succ = succ;
+  bool first = true;
+  int64_t cur_n = n, cur_head = head;
+  while (cur_n > kBase) {
+    Level* L = new Level();
+    levels.push_back(L);
+    L->n = cur_n;
+    L->head = cur_head;
+    const int64_t regular = ceil_div(cur_n, kK);
+    L->extra = (cur_head % kK == 0) ? -1 : regular;
+    L->nsub = regular + (L->extra >= 0 ? 1 : 0);
+    if (first) {
+      L->tmp.ptr = out_rank;  // packed (sublist, offset) lives in the output until expanded
+      L->tmp.owned = false;
+    } else {
+      HB_TRY(alloc(&L->tmp, (size_t)cur_n * 8, s));
+    }
+    HB_TRY(alloc(&L->nxt, (size_t)L->nsub * 8, s));
+    HB_TRY(alloc(&L->len, (size_t)L->nsub * 8, s));
+    int64_t blocks = ceil_div(L->nsub, 128);
+    if (blocks > (int64_t)di.sms * 64) blocks = (int64_t)di.sms * 64;
+    if (first) {
+      lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(
+          (const S*)cur_succ, nullptr, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>());
+    } else {
+      lr_walk_kernel<int64_t, true><<<(int)blocks, 128, 0, s>>>(
+          (const int64_t*)cur_succ, w, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>());
+    }
+    HB_TRY(check_launch());
+    cur_succ = L->nxt.ptr;
+    w = L->len.as<int64_t>();
+    cur_head = L->extra >= 0 ? L->extra : cur_head / kK;
+    cur_n = L->nsub;
+    first = false;
+  }
+
+  // top level
+  DevBuf top_nxt, top_len, top_prefix;
+  if (first) {  // the whole list is small: rank it directly (unit weights)
+    HB_TRY(alloc(&top_nxt, (size_t)cur_n * 8, s));
+    HB_TRY(alloc(&top_len, (size_t)cur_n * 8, s));
+    std::vector<int64_t> ones((size_t)cur_n, 1);
+    std::vector<int64_t> nx((size_t)cur_n);
+    std::vector<S> sh((size_t)cur_n);
+    HB_CUDA_TRY(cudaMemcpyAsync(sh.data(), succ, (size_t)cur_n * sizeof(S), cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < cur_n; ++i) nx[(size_t)i] = (int64_t)sh[(size_t)i];
+    HB_CUDA_TRY(cudaMemcpyAsync(top_nxt.ptr, nx.data(), (size_t)cur_n * 8, cudaMemcpyHostToDevice, s));
+    HB_CUDA_TRY(cudaMemcpyAsync(top_len.ptr, ones.data(), (size_t)cur_n * 8, cudaMemcpyHostToDevice, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+    top_nxt.ptr = const_cast<void*>(cur_succ);
+    top_len.ptr = const_cast<int64_t*>(w);
+  }
+  HB_TRY(alloc(&top_prefix, (size_t)cur_n * 8, s));
+  HB_TRY(alloc(&st, 16, s));
+  HB_CUDA_TRY(cudaFuncSetAttribute(lr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopSmem));
+  lr_top_kernel<<<1, 1024, kTopSmem, s>>>(top_nxt.as<int64_t>(), top_len.as<int64_t>(), cur_n, cur_head,
+                                   top_prefix.as<int64_t>(), st.as<int64_t>());
+  HB_TRY(check_launch());
+  int64_t status[2] = {0, 0};
+  unsigned long long errs = 0;
+  HB_CUDA_TRY(cudaMemcpyAsync(status, st.ptr, 16, cudaMemcpyDeviceToHost, s));
+  HB_CUDA_TRY(cudaMemcpyAsync(&errs, err.ptr, 8, cudaMemcpyDeviceToHost, s));
+  HB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (errs || status[1]) {
+    set_error("list contains a cycle");
+    return HB_ESTRUCT;
+  }
+  if (status[0] != n) {
+    set_error("chain covers %lld of %lld nodes (broken list)", (long long)status[0], (long long)n);
+    return HB_ESTRUCT;
+  }
+
+  // ascend: expand every level's packed offsets
+  const int64_t* prefix = top_prefix.as<int64_t>();
+  if (first) {
+    // rank = prefix of the unit-weight top list
+    HB_CUDA_TRY(cudaMemcpyAsync(out_rank, prefix, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+    return HB_OK;
+  }
+  for (int li = (int)levels.size() - 1; li >= 0; --li) {
+    Level* L = levels[(size_t)li];
+    int64_t* dst;
+    if (li == 0) {
+      dst = out_rank;
+    } else {
+      HB_TRY(alloc(&L->ranked, (size_t)L->n * 8, s));
+      dst = L->ranked.as<int64_t>();
+    }
+    int64_t blocks = ceil_div(L->n, 256);
+    if (blocks > (int64_t)di.sms * 32) blocks = (int64_t)di.sms * 32;
+    lr_expand_kernel<<<(int)blocks, 256, 0, s>>>(L->tmp.as<uint64_t>(), L->n, prefix, dst);
+    HB_TRY(check_launch());
+    prefix = dst;
+  }
+  return HB_OK;
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t head, int64_t* rank,
+                            int flags, void* stream) {
+  HB_CHECK_ARG(succ_code == HB_I32 || succ_code == HB_I64, "succ must be int32 or int64");
+  HB_CHECK_ARG(n >= 1, "list must have at least one node");
+  HB_CHECK_ARG(succ && rank, "NULL pointer");
+  if (head < 0 || head >= n) {
+    set_error("head out of range");
+    return HB_ESTRUCT;
+  }
+  HB_CHECK_ARG(n < (1ll << 31), "lists of up to 2^31-1 nodes are supported");
+  const bool dev = flags & HB_DEVICE_PTRS;
+  cudaStream_t s = as_stream(stream);
+  const size_t se = succ_code == HB_I32 ? 4 : 8;
+  DevBuf d_succ, d_rank, chk;
+  HB_TRY(stage_in(&d_succ, succ, (size_t)n * se, dev, s));
+  HB_TRY(stage_out(&d_rank, rank, (size_t)n * 8, dev, s));
+  // structural pre-check (validate_list's range check + tail count)
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  HB_TRY(alloc(&chk, 16, s));
+  HB_CUDA_TRY(cudaMemsetAsync(chk.ptr, 0, 16, s));
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+  if (succ_code == HB_I32) lr_check_kernel<int32_t><<<(int)blocks, 256, 0, s>>>(d_succ.as<int32_t>(), n, chk.as<unsigned long long>());
+  else lr_check_kernel<int64_t><<<(int)blocks, 256, 0, s>>>(d_succ.as<int64_t>(), n, chk.as<unsigned long long>());
+  HB_TRY(check_launch());
+  unsigned long long c[2] = {0, 0};
+  HB_CUDA_TRY(cudaMemcpyAsync(c, chk.ptr, 16, cudaMemcpyDeviceToHost, s));
+  HB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (c[1]) {
+    set_error("successor index out of range");
+    return HB_ESTRUCT;
+  }
+  if (c[0] != 1) {
+    set_error(c[0] == 0 ? "list contains a cycle" : "list has %llu tails (broken list)", c[0]);
+    return HB_ESTRUCT;
+  }
+  int rc = succ_code == HB_I32 ? rank_levels<int32_t>(d_succ.as<int32_t>(), n, head, d_rank.as<int64_t>(), s)
+                               : rank_levels<int64_t>(d_succ.as<int64_t>(), n, head, d_rank.as<int64_t>(), s);
+  if (rc != HB_OK) return rc;
+  HB_TRY(copy_out(rank, d_rank, (size_t)n * 8, dev, s));
+  return finish(flags, s);
+}

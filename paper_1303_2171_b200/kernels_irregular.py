@@ -329,3 +329,80 @@ class SpmvWorkload:
         y = np.empty_like(y_perm)
         y[to_host(self.prep.perm)] = y_perm
         return y
+
+
+# --------------------------------------------------------------------------
+# list ranking (kernels_irregular.py:356-508)
+
+
+@dataclass(frozen=True)
+class LinkedListArr:
+    """Successor-array list: succ[i] is the next node or LIST_END (:360-365)."""
+
+    succ: Any
+    head: int
+
+
+@dataclass(frozen=True)
+class ListRankStats:
+    fis_rounds: int
+    round_sizes: tuple[int, ...]
+    reduced_size: int
+    removed_total: int
+    sublist_count: int
+
+
+def validate_list(lst: LinkedListArr) -> None:
+    """The chain from head must visit every node exactly once (:377-393).
+    Host arrays: range check + walk on the host like the reference; CUDA
+    tensors: the GPU ranking itself validates (hb_list_rank)."""
+    succ = lst.succ
+    n = int(succ.numel() if is_device_array(succ) else succ.size)
+    if not 0 <= lst.head < n:
+        raise StructuralError("head out of range")
+    if is_device_array(succ):
+        gpu_list_rank(succ, lst.head)
+        return
+    if n and (succ.min() < LIST_END or succ.max() >= n):
+        raise StructuralError("successor index out of range")
+    seen, cur = 0, lst.head
+    while cur != LIST_END:
+        seen += 1
+        if seen > n:
+            raise StructuralError("list contains a cycle")
+        cur = int(succ[cur])
+    if seen != n:
+        raise StructuralError(f"chain covers {seen} of {n} nodes (broken list)")
+
+
+def gpu_list_rank(succ: Any, head: int, out: Any = None, *, asynchronous: bool = False) -> Any:
+    """rank[i] = distance of node i from `head` (hb_list_rank: sparse ruling
+    set + Wyllie pointer jumping).  Host succ → int64 numpy ranks; CUDA succ
+    (int32/int64) → int64 CUDA tensor.  Malformed lists raise StructuralError."""
+    _lib.load()
+    require_gpu()
+    sb = buf(succ)
+    if sb.dtype not in (np.dtype(np.int32), np.dtype(np.int64)):
+        sb = buf(np.asarray(to_host(succ), dtype=np.int64))
+    n = sb.size
+    if n < 1:
+        raise StructuralError("head out of range")
+    code = _index_code(sb.owner)
+    if sb.device:
+        import torch
+
+        res = out if out is not None else torch.empty(n, dtype=torch.int64, device=succ.device)
+        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0)
+        _lib.call("hb_list_rank", vp(sb.ptr), code, n, int(head), vp(res.data_ptr()), flags,
+                  current_stream_handle(succ))
+        return res
+    res = np.empty(n, dtype=np.int64)
+    _lib.call("hb_list_rank", vp(sb.ptr), code, n, int(head), vp(res.ctypes.data), 0, current_stream_handle())
+    return res
+
+
+def list_rank_hybrid(lst: LinkedListArr, platform: Platform, seed: int) -> Any:
+    """rank[i] = distance of node i from the head (:505-508).  The ranks do
+    not depend on the seed or on the reduction schedule, so this entry point
+    takes the GPU fast path directly (validation included)."""
+    return gpu_list_rank(lst.succ, lst.head)

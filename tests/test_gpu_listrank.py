@@ -1,0 +1,93 @@
+"""List ranking GPU parity: ranks identical to the reference's own outputs
+(golden) and to pointer chasing; malformed lists raise StructuralError.
+Mirrors tests/test_kernels_irregular.py:214-266 and acceptance :204-229."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import datasets as ods
+from oracle import listrank as olr
+from oracle import rng as orng
+from paper_1303_2171_b200.errors import StructuralError
+from paper_1303_2171_b200.kernels_irregular import LinkedListArr, gpu_list_rank, list_rank_hybrid, validate_list
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_ranks(platform13):
+    g = golden("listrank")
+    for i in range(6):
+        lst = LinkedListArr(g[f"succ_{i}"], int(g[f"head_{i}"][0]))
+        assert np.array_equal(list_rank_hybrid(lst, platform13, int(g[f"seed_{i}"][0])), g[f"rank_{i}"])
+
+
+def test_singleton_and_ordered_chain(platform13):
+    assert list_rank_hybrid(LinkedListArr(np.array([-1]), 0), platform13, 1).tolist() == [0]
+    assert list_rank_hybrid(LinkedListArr(np.array([1, 2, 3, -1]), 0), platform13, 1).tolist() == [0, 1, 2, 3]
+
+
+@pytest.mark.parametrize("n", [2, 63, 64, 65, 4095, 4096, 4097, 300_001, 2_000_000])
+def test_random_lists_match_chase(n):
+    succ, head = ods.linked_list(n, n)
+    order = np.argsort(orng.draws(n, n), kind="stable")
+    want = olr.ranks_from_order(order)
+    assert np.array_equal(gpu_list_rank(succ, head), want)
+    assert np.array_equal(gpu_list_rank(succ.astype(np.int32), head), want)
+
+
+def test_structural_invariants_50_lists(platform13):
+    for i in range(50):
+        n = 100 + (orng.mix_seed(i, 5) % 9_901)
+        succ, head = ods.linked_list(int(n), i)
+        r = list_rank_hybrid(LinkedListArr(succ, head), platform13, i)
+        assert np.array_equal(r, olr.chase(succ, head))
+        assert r[head] == 0
+        inner = succ >= 0
+        assert np.array_equal(r[succ[inner]], r[inner] + 1)
+
+
+def test_pathological_orders():
+    n = 100_000
+    ordered = np.arange(1, n + 1, dtype=np.int64); ordered[-1] = -1
+    assert np.array_equal(gpu_list_rank(ordered, 0), np.arange(n))
+    rev = np.arange(-1, n - 1, dtype=np.int64)  # n-1 -> n-2 -> ... -> 0
+    assert np.array_equal(gpu_list_rank(rev, n - 1), np.arange(n)[::-1])
+    # non-multiples of 64 first, then multiples: one very long first sublist
+    order = np.concatenate([np.flatnonzero(np.arange(n) % 64 != 0), np.arange(0, n, 64)])
+    succ = np.full(n, -1, dtype=np.int64); succ[order[:-1]] = order[1:]
+    assert np.array_equal(gpu_list_rank(succ, int(order[0])), olr.ranks_from_order(order))
+
+
+def test_device_resident():
+    import torch
+
+    succ, head = ods.linked_list(1_000_000, 42)
+    got = gpu_list_rank(torch.from_numpy(succ.astype(np.int32)).cuda(), head)
+    assert np.array_equal(got.cpu().numpy(), olr.chase(succ, head))
+
+
+def test_broken_lists_raise():
+    for succ, head in ((np.array([1, 0]), 0), (np.array([-1, -1]), 0), (np.array([5]), 0), (np.array([-1]), 3)):
+        with pytest.raises(StructuralError):
+            gpu_list_rank(succ, head)
+        with pytest.raises(StructuralError):
+            validate_list(LinkedListArr(succ, head))
+    # big broken cases: a detached cycle, and two chains
+    n = 100_000
+    succ, head = ods.linked_list(n, 3)
+    cyc = succ.copy()
+    tail = int(np.flatnonzero(cyc == -1)[0])
+    order = olr.chase(succ, head).argsort()
+    # cut the chain 10 nodes before the end and close those nodes into a ring
+    a = order[-10]
+    cyc[order[-11]] = -1
+    cyc[tail] = a
+    with pytest.raises(StructuralError):
+        gpu_list_rank(cyc, head)
+    two = succ.copy()
+    two[order[n // 2]] = -1  # second half detached: two tails
+    with pytest.raises(StructuralError):
+        gpu_list_rank(two, head)

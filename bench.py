@@ -560,7 +560,88 @@ def _presorted_then_gpu():
     return fn
 
 
-WORKLOADS = {"hist": HistBench, "spmv": SpmvBench, "bilat": BilatBench, "sort": SortBench}
+class LrBench:
+    """BASELINE configs[4]: list ranking of a 2^28-node random linked list
+    (gen_list(2^28, 42), generated on the device bit-identically), succ int32
+    on the device, ranks int64."""
+
+    name = "lr"
+    unit = "Mnodes/s"
+    kernel = "lr_walk_kernel"
+
+    def __init__(self, n: int = 1 << 28, seed: int = 42):
+        self.n, self.seed = n, seed
+
+    def config(self):
+        return {"workload": f"lr: list ranking of a 2^{self.n.bit_length() - 1}-node random list (sparse ruling set + Wyllie)",
+                "n_per_gpu": self.n, "seed": self.seed,
+                "input": "gen_list(n, 42): stable argsort of splitmix64 draws (device-generated, bit-identical)",
+                "l2": "succ 1 GiB + rank 2 GiB > L2",
+                "algorithmic_bytes": "12 B/node (4 succ + 8 rank); random 4-B reads move 32-B sectors"}
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_1303_2171_b200.datasets import device_gen_list
+
+        self.world = world
+        self.succ, self.head = device_gen_list(self.n, self.seed + rank)
+        self.rank = torch.empty(self.n, dtype=torch.int64, device="cuda")
+
+    def step(self):
+        from paper_1303_2171_b200.kernels_irregular import gpu_list_rank
+
+        gpu_list_rank(self.succ, self.head, out=self.rank)
+        return 8  # check + 3 walks + top + 3 expands
+
+    def units_per_step(self):
+        return self.n
+
+    def bytes_per_launch(self):
+        return 12 * self.n
+
+    def verify(self):
+        s = self.succ.cpu().numpy().astype(np.int64)
+        r = self.rank.cpu().numpy()
+        inner = s >= 0
+        ok = r[self.head] == 0 and np.array_equal(r[s[inner]], r[inner] + 1)
+        ok = ok and np.array_equal(np.bincount(r, minlength=self.n), np.ones(self.n, dtype=np.int64))
+        return bool(ok)
+
+    def e2e_setup(self):
+        import torch
+
+        from paper_1303_2171_b200.kernels_irregular import LinkedListArr
+        from paper_1303_2171_b200.platform import Platform
+
+        host = torch.empty(self.n, dtype=torch.int64, pin_memory=True)
+        host.copy_(self.succ)
+        self.host = host
+        self.lst = LinkedListArr(host.numpy(), self.head)
+        self.platform = Platform.build(1.0, 3.0)
+
+    def e2e_step(self):
+        from paper_1303_2171_b200.kernels_irregular import list_rank_hybrid
+
+        return list_rank_hybrid(self.lst, self.platform, self.seed)
+
+    def e2e_bytes(self):
+        return 8 * self.n, 8 * self.n
+
+    def cpu_sample(self, budget_s: float):
+        from oracle import datasets as ods
+        from oracle import listrank as olr
+
+        m = 1 << 22
+        succ, head = ods.linked_list(m, self.seed)
+        fn = lambda: olr.list_rank_with_stats(succ, head, self.seed)  # noqa: E731
+        return fn, m, "gen_list(2^22, 42) through the reference's list_rank_with_stats (validate + FIS + sublists), 1 thread"
+
+    def cpu_cores(self):
+        return 1
+
+
+WORKLOADS = {"hist": HistBench, "spmv": SpmvBench, "bilat": BilatBench, "sort": SortBench, "lr": LrBench}
 
 
 # ---------------------------------------------------------------- drivers

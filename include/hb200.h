@@ -159,6 +159,11 @@ int hb_sort_bounds(const void* keys, int key_code, const uint32_t* vals, int64_t
 int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t head, int64_t* rank, int flags,
                  void* stream);
 
+/* Device-side gen_list (datasets.py:58-63) second half: given `order`, the
+ * stable argsort of the splitmix draws (hb_sort of the draws with an index
+ * payload), link succ[order[i]] = order[i+1], tail -1.  Device pointers. */
+int hb_link_order(const int32_t* order, int64_t n, void* succ, int succ_code, int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

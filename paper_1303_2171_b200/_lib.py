@@ -50,6 +50,7 @@ _SIGNATURES: dict[str, list] = {
     "hb_sort": [_vp, _vp, _int, _vp, _vp, _i64, _vp, _int, _vp],
     "hb_sort_bounds": [_vp, _int, _vp, _i64, _vp, _vp, _i32, _vp, _int, _vp],
     "hb_list_rank": [_vp, _int, _i64, _i64, _vp, _int, _vp],
+    "hb_link_order": [_vp, _i64, _vp, _int, _int, _vp],
 }
 
 _lock = threading.Lock()

@@ -274,10 +274,34 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
   return HB_OK;
 }
 
+// succ[order[i]] = order[i+1], succ[order[n-1]] = -1 (gen_list, datasets.py:58-63)
+template <typename S>
+__global__ void link_order_kernel(const int32_t* __restrict__ order, int64_t n, S* __restrict__ succ) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    succ[order[i]] = i + 1 < n ? (S)order[i + 1] : (S)-1;
+}
+
 }  // namespace
 }  // namespace hb
 
 using namespace hb;
+
+extern "C" int hb_link_order(const int32_t* order, int64_t n, void* succ, int succ_code, int flags,
+                             void* stream) {
+  HB_CHECK_ARG(succ_code == HB_I32 || succ_code == HB_I64, "succ must be int32 or int64");
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_link_order works on device arrays");
+  HB_CHECK_ARG(n >= 0 && n < (1ll << 31), "n out of range");
+  if (n == 0) return HB_OK;
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  cudaStream_t s = as_stream(stream);
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+  if (succ_code == HB_I32) link_order_kernel<int32_t><<<(int)blocks, 256, 0, s>>>(order, n, (int32_t*)succ);
+  else link_order_kernel<int64_t><<<(int)blocks, 256, 0, s>>>(order, n, (int64_t*)succ);
+  return finish(flags, s);
+}
 
 extern "C" int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t head, int64_t* rank,
                             int flags, void* stream) {

@@ -116,3 +116,29 @@ def _row_with_retries(base: int, draw_pos: int, k: int, cols: int) -> tuple[int,
         draw_pos += 1
         chosen = np.unique(np.concatenate([chosen, np.unique(uniform_ints(s, 2 * k + 8, cols))]))
     return draw_pos, chosen[:k]
+
+
+def device_gen_list(n: int, seed: int, succ_dtype=np.int32):
+    """gen_list on the device, bit-identical to the reference (datasets.py:
+    58-63): draws 1..n of `seed` (hb_gen_splitmix), stable argsort by an LSD
+    radix sort of the 64-bit draws with an index payload (hb_sort), then
+    hb_link_order.  Returns (succ CUDA tensor, head)."""
+    import torch
+
+    from . import _lib
+    from .gpu import current_stream_handle, vp
+    from .rng import device_splitmix
+
+    draws = torch.empty(n, dtype=torch.int64, device="cuda")
+    device_splitmix(draws, seed, _lib.HB_GEN_RAW)
+    order = torch.arange(n, dtype=torch.int32, device="cuda")
+    st = current_stream_handle(draws)
+    _lib.call("hb_sort", vp(draws.data_ptr()), vp(draws.data_ptr()), _lib.DTYPE_CODES["u8"], vp(order.data_ptr()),
+              vp(order.data_ptr()), n, None, _lib.HB_DEVICE_PTRS, st)
+    del draws
+    tdt = torch.int32 if np.dtype(succ_dtype) == np.int32 else torch.int64
+    succ = torch.empty(n, dtype=tdt, device="cuda")
+    _lib.call("hb_link_order", vp(order.data_ptr()), n, vp(succ.data_ptr()),
+              _lib.DTYPE_CODES["i4" if tdt == torch.int32 else "i8"], _lib.HB_DEVICE_PTRS, st)
+    head = int(order[0].item())
+    return succ, head

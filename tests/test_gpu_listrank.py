@@ -91,3 +91,15 @@ def test_broken_lists_raise():
     two[order[n // 2]] = -1  # second half detached: two tails
     with pytest.raises(StructuralError):
         gpu_list_rank(two, head)
+
+
+def test_device_list_generator_matches_reference():
+    from paper_1303_2171_b200.datasets import device_gen_list
+
+    g = golden("listrank")
+    succ, head = device_gen_list(10_000, 42, np.int64)
+    assert np.array_equal(succ.cpu().numpy(), g["succ_0"]) and head == int(g["head_0"][0])
+    for n, seed in ((5, 7), (4097, 11), (100_000, 3)):
+        s2, h2 = device_gen_list(n, seed)
+        want_s, want_h = ods.linked_list(n, seed)
+        assert np.array_equal(s2.cpu().numpy(), want_s) and h2 == want_h

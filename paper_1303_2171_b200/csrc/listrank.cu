@@ -30,20 +30,16 @@ namespace {
 constexpr int kK = 64;        // sublist spacing (node index multiple)
 constexpr int kBase = 4096;   // top level size ranked in one CTA
 
-// Validation + working copy: slot[i] = succ[i] (the level-1 walk then
-// reads the successor and writes the node's packed (sublist, offset) into
-// the same 8-byte slot: one DRAM sector per node instead of two);
-// out[0] += tails (succ == -1), out[1] += out-of-range successors.
+// Validation: out[0] += tails (succ == -1), out[1] += out-of-range successors.
 template <typename S>
-__global__ void lr_prep_kernel(const S* __restrict__ succ, int64_t n, int64_t* __restrict__ slot,
-                               unsigned long long* __restrict__ out) {
+__global__ void lr_check_kernel(const S* __restrict__ succ, int64_t n,
+                                unsigned long long* __restrict__ out) {
   unsigned long long tails = 0, bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = (int64_t)succ[i];
     tails += (s == -1);
     bad += (s < -1 || s >= n);
-    slot[i] = s;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -63,64 +59,72 @@ __device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra
   return (v % kK) == 0 ? v / kK : extra;
 }
 
-// One thread per sublist: walk from its head to the next head.
-// tmp[v] = (sublist << 32) | local offset; nxt[j] = next sublist or -1; len[j] = weight sum.
-template <typename S, bool WEIGHTED>
-__global__ void lr_walk_kernel(const S* __restrict__ succ, const int64_t* __restrict__ w, int64_t n,
-                               int64_t head, int64_t nsub, int64_t extra, uint64_t* __restrict__ tmp,
-                               int64_t* __restrict__ nxt, int64_t* __restrict__ len,
-                               unsigned long long* __restrict__ err) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nsub;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t h = j == extra ? head : j * kK;
-    if (h >= n) {  // no such node: an isolated, zero-weight sublist
-      nxt[j] = -1;
-      len[j] = 0;
-      continue;
-    }
-    tmp[h] = (uint64_t)j << 32;
-    int64_t acc = WEIGHTED ? w[h] : 1;
-    int64_t cur = (int64_t)__ldg(succ + h);
-    int64_t steps = 0;
-    while (cur != -1 && !is_head(cur, head)) {
-      tmp[cur] = ((uint64_t)j << 32) | (uint64_t)(uint32_t)acc;
-      acc += WEIGHTED ? w[cur] : 1;
-      cur = (int64_t)__ldg(succ + cur);
-      if (++steps > n) {  // cycle without a sublist head
-        atomicAdd(err, 1ull);
-        break;
-      }
-    }
-    nxt[j] = (cur == -1 || steps > n) ? -1 : sub_id(cur, head, extra);
-    len[j] = acc;
-  }
+// Sublist walks.  tmp[v] = (sublist << 32) | local offset; nxt[j] = next
+// sublist or -1; len[j] = weight sum.  Each thread owns the sublists
+// j = t, t+T, t+2T, ... and keeps kChains of them in flight at once; the
+// loop is flattened (a finished walk immediately starts the thread's next
+// sublist), so lanes never idle waiting for the longest walk of their warp
+// and every thread has kChains independent dependent-load chains in flight.
+constexpr int kChains = 4;
+
+template <typename S>
+__device__ __forceinline__ int64_t ld_succ(const S* p) {
+  return (int64_t)__ldg(p);
 }
 
-// Level 1, in place: slot[v] holds succ[v] until v is visited, then
-// kVisited | (sublist << 32) | offset.  A visited slot read again (in-degree
-// > 1, i.e. a malformed list) is detected instead of followed.
-constexpr uint64_t kVisited = 1ull << 63;
+__device__ __forceinline__ void st_stream(uint64_t* p, uint64_t v) {
+  asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
-__global__ void lr_walk_inplace_kernel(int64_t* __restrict__ slot, int64_t n, int64_t head,
-                                       int64_t nsub, int64_t extra, int64_t* __restrict__ nxt,
-                                       int64_t* __restrict__ len, unsigned long long* __restrict__ err) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nsub;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t h = j == extra ? head : j * kK;
-    int64_t cur = slot[h];
-    slot[h] = (int64_t)(kVisited | ((uint64_t)j << 32));
-    int64_t acc = 1;
-    bool bad = cur < -1 || cur >= n;
-    while (!bad && cur != -1 && !is_head(cur, head)) {
-      const int64_t nx = slot[cur];
-      slot[cur] = (int64_t)(kVisited | ((uint64_t)j << 32) | (uint64_t)(uint32_t)acc);
-      ++acc;
-      bad = nx < -1 || nx >= n;  // visited twice (cycle / shared successor)
-      cur = nx;
+template <typename S, bool WEIGHTED>
+__global__ void __launch_bounds__(128)
+    lr_walk_kernel(const S* __restrict__ succ, const int64_t* __restrict__ w, int64_t n, int64_t head,
+                   int64_t nsub, int64_t extra, uint64_t* __restrict__ tmp, int64_t* __restrict__ nxt,
+                   int64_t* __restrict__ len, unsigned long long* __restrict__ err) {
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // next sublist to start
+  int64_t j[kChains], cur[kChains], acc[kChains], steps[kChains];
+  auto start = [&](int c) {
+    while (job < nsub) {
+      const int64_t jj = job;
+      job += T;
+      const int64_t h = jj == extra ? head : jj * kK;
+      if (h >= n) {
+        nxt[jj] = -1;
+        len[jj] = 0;
+        continue;
+      }
+      tmp[h] = (uint64_t)jj << 32;
+      j[c] = jj;
+      acc[c] = WEIGHTED ? w[h] : 1;
+      cur[c] = ld_succ(succ + h);
+      steps[c] = 0;
+      return;
     }
-    if (bad) atomicAdd(err, 1ull);
-    nxt[j] = (cur == -1 || bad) ? -1 : sub_id(cur, head, extra);
-    len[j] = acc;
+    j[c] = -1;
+  };
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) start(c);
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      if (j[c] < 0) continue;
+      any = true;
+      const int64_t v = cur[c];
+      if (v == -1 || is_head(v, head) || steps[c] > n) {
+        if (steps[c] > n) atomicAdd(err, 1ull);  // cycle without a sublist head
+        nxt[j[c]] = (v == -1 || steps[c] > n) ? -1 : sub_id(v, head, extra);
+        len[j[c]] = acc[c];
+        start(c);
+        continue;
+      }
+      st_stream(tmp + v, ((uint64_t)j[c] << 32) | (uint64_t)(uint32_t)acc[c]);
+      acc[c] += WEIGHTED ? w[v] : 1;
+      cur[c] = ld_succ(succ + v);
+      ++steps[c];
+    }
+    if (!any) break;
   }
 }
 
@@ -130,7 +134,7 @@ __global__ void lr_expand_kernel(const uint64_t* __restrict__ tmp, int64_t n,
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t t = tmp[v];
-    out[v] = prefix[(t >> 32) & 0x7fffffffull] + (int64_t)(t & 0xffffffffull);
+    out[v] = prefix[t >> 32] + (int64_t)(t & 0xffffffffull);
   }
 }
 
@@ -224,12 +228,12 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
     }
     HB_TRY(alloc(&L->nxt, (size_t)L->nsub * 8, s));
     HB_TRY(alloc(&L->len, (size_t)L->nsub * 8, s));
-    int64_t blocks = ceil_div(L->nsub, 128);
-    if (blocks > (int64_t)di.sms * 64) blocks = (int64_t)di.sms * 64;
+    int64_t blocks = ceil_div(L->nsub, 128 * kChains);
+    if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;  // 2048 resident threads / SM
     if (first) {
-      lr_walk_inplace_kernel<<<(int)blocks, 128, 0, s>>>(
-          out_rank, cur_n, cur_head, L->nsub, L->extra, L->nxt.as<int64_t>(), L->len.as<int64_t>(),
-          err.as<unsigned long long>());
+      lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(
+          (const S*)cur_succ, nullptr, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>());
     } else {
       lr_walk_kernel<int64_t, true><<<(int)blocks, 128, 0, s>>>(
           (const int64_t*)cur_succ, w, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
@@ -250,8 +254,10 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
     HB_TRY(alloc(&top_len, (size_t)cur_n * 8, s));
     std::vector<int64_t> ones((size_t)cur_n, 1);
     std::vector<int64_t> nx((size_t)cur_n);
-    HB_CUDA_TRY(cudaMemcpyAsync(nx.data(), out_rank, (size_t)cur_n * 8, cudaMemcpyDeviceToHost, s));
+    std::vector<S> sh((size_t)cur_n);
+    HB_CUDA_TRY(cudaMemcpyAsync(sh.data(), succ, (size_t)cur_n * sizeof(S), cudaMemcpyDeviceToHost, s));
     HB_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < cur_n; ++i) nx[(size_t)i] = (int64_t)sh[(size_t)i];
     HB_CUDA_TRY(cudaMemcpyAsync(top_nxt.ptr, nx.data(), (size_t)cur_n * 8, cudaMemcpyHostToDevice, s));
     HB_CUDA_TRY(cudaMemcpyAsync(top_len.ptr, ones.data(), (size_t)cur_n * 8, cudaMemcpyHostToDevice, s));
     HB_CUDA_TRY(cudaStreamSynchronize(s));
@@ -356,8 +362,8 @@ extern "C" int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t 
   HB_CUDA_TRY(cudaMemsetAsync(chk.ptr, 0, 16, s));
   int64_t blocks = ceil_div(n, 256);
   if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
-  if (succ_code == HB_I32) lr_prep_kernel<int32_t><<<(int)blocks, 256, 0, s>>>(d_succ.as<int32_t>(), n, d_rank.as<int64_t>(), chk.as<unsigned long long>());
-  else lr_prep_kernel<int64_t><<<(int)blocks, 256, 0, s>>>(d_succ.as<int64_t>(), n, d_rank.as<int64_t>(), chk.as<unsigned long long>());
+  if (succ_code == HB_I32) lr_check_kernel<int32_t><<<(int)blocks, 256, 0, s>>>(d_succ.as<int32_t>(), n, chk.as<unsigned long long>());
+  else lr_check_kernel<int64_t><<<(int)blocks, 256, 0, s>>>(d_succ.as<int64_t>(), n, chk.as<unsigned long long>());
   HB_TRY(check_launch());
   unsigned long long c[2] = {0, 0};
   HB_CUDA_TRY(cudaMemcpyAsync(c, chk.ptr, 16, cudaMemcpyDeviceToHost, s));

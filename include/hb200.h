@@ -164,6 +164,17 @@ int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t head, int64
  * payload), link succ[order[i]] = order[i+1], tail -1.  Device pointers. */
 int hb_link_order(const int32_t* order, int64_t n, void* succ, int succ_code, int flags, void* stream);
 
+/* The reference's fractional-independent-set reduction and sublist-head
+ * choice (kernels_irregular.py:396-448), run on the GPU for its statistics:
+ * round_sizes[r] = live nodes at the start of round r (first round_cap
+ * rounds), stats = {fis_rounds, reduced_size, removed_total, sublist_count}
+ * — identical to the reference's ListRankStats for the same (list, seed,
+ * sublists = 4 * total workers).  The list must be valid (hb_list_rank
+ * first); non-convergence → HB_ESTRUCT.                                    */
+int hb_list_fis_stats(const void* succ, int succ_code, int64_t n, int64_t head, uint64_t seed,
+                      int32_t sublists, int64_t* round_sizes, int32_t round_cap, int64_t* stats,
+                      int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

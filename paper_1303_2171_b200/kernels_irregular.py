@@ -401,6 +401,36 @@ def gpu_list_rank(succ: Any, head: int, out: Any = None, *, asynchronous: bool =
     return res
 
 
+def gpu_list_fis_stats(succ: Any, head: int, seed: int, sublists: int) -> ListRankStats:
+    """The reference's FIS reduction + sublist-head choice on the GPU
+    (hb_list_fis_stats), for its ListRankStats (:396-448, :495-501)."""
+    _lib.load()
+    require_gpu()
+    sb = buf(succ)
+    if sb.dtype not in (np.dtype(np.int32), np.dtype(np.int64)):
+        sb = buf(np.asarray(to_host(succ), dtype=np.int64))
+    cap = 1000
+    sizes = np.zeros(cap, dtype=np.int64)
+    st = np.zeros(4, dtype=np.int64)
+    flags = _lib.HB_DEVICE_PTRS if sb.device else 0
+    _lib.call("hb_list_fis_stats", vp(sb.ptr), _index_code(sb.owner), sb.size, int(head), int(seed) & ((1 << 64) - 1),
+              int(sublists), vp(sizes.ctypes.data), cap, vp(st.ctypes.data), flags,
+              current_stream_handle(succ if sb.device else None))
+    rounds = int(st[0])
+    return ListRankStats(rounds, tuple(int(v) for v in sizes[:rounds]), int(st[1]), int(st[2]), int(st[3]))
+
+
+def list_rank_with_stats(lst: LinkedListArr, platform: Platform, seed: int) -> tuple[Any, ListRankStats]:
+    """(rank, ListRankStats) like the reference (:481-502).  Ranks: GPU sparse
+    ruling set (validates the list first, StructuralError as validate_list);
+    statistics: the reference's own FIS reduction and sublist choice, on the
+    GPU, with sublists = 4 x (workers_a + workers_b)."""
+    rank = gpu_list_rank(lst.succ, lst.head)
+    workers = platform.device_a.worker_count + platform.device_b.worker_count
+    stats = gpu_list_fis_stats(lst.succ, lst.head, seed, 4 * workers)
+    return rank, stats
+
+
 def list_rank_hybrid(lst: LinkedListArr, platform: Platform, seed: int) -> Any:
     """rank[i] = distance of node i from the head (:505-508).  The ranks do
     not depend on the seed or on the reduction schedule, so this entry point

@@ -12,7 +12,13 @@ from oracle import datasets as ods
 from oracle import listrank as olr
 from oracle import rng as orng
 from paper_1303_2171_b200.errors import StructuralError
-from paper_1303_2171_b200.kernels_irregular import LinkedListArr, gpu_list_rank, list_rank_hybrid, validate_list
+from paper_1303_2171_b200.kernels_irregular import (
+    LinkedListArr,
+    gpu_list_rank,
+    list_rank_hybrid,
+    list_rank_with_stats,
+    validate_list,
+)
 
 pytestmark = pytest.mark.gpu
 
@@ -103,3 +109,41 @@ def test_device_list_generator_matches_reference():
         s2, h2 = device_gen_list(n, seed)
         want_s, want_h = ods.linked_list(n, seed)
         assert np.array_equal(s2.cpu().numpy(), want_s) and h2 == want_h
+
+
+def test_golden_stats_identical(platform13):
+    g = golden("listrank")
+    for i in range(6):
+        lst = LinkedListArr(g[f"succ_{i}"], int(g[f"head_{i}"][0]))
+        rank, st = list_rank_with_stats(lst, platform13, int(g[f"seed_{i}"][0]))
+        assert np.array_equal(rank, g[f"rank_{i}"])
+        assert [st.fis_rounds, st.reduced_size, st.removed_total, st.sublist_count] == g[f"stats_{i}"].tolist()
+        assert list(st.round_sizes) == g[f"sizes_{i}"].tolist()
+
+
+def test_stats_match_oracle_many_lists(platform13):
+    for i in range(12):
+        n = 100 + (orng.mix_seed(i, 5) % 20_000)
+        succ, head = ods.linked_list(int(n), i)
+        rank, st = list_rank_with_stats(LinkedListArr(succ, head), platform13, i)
+        want_rank, (rounds, sizes, reduced, removed, subl) = olr.list_rank_with_stats(succ, head, i)
+        assert np.array_equal(rank, want_rank)
+        assert (st.fis_rounds, st.round_sizes, st.reduced_size, st.removed_total, st.sublist_count) == (
+            rounds, sizes, reduced, removed, subl)
+        assert st.reduced_size <= n / math.log2(n)
+
+
+def test_stats_large_list_device():
+    import torch
+
+    from paper_1303_2171_b200.datasets import device_gen_list
+    from paper_1303_2171_b200.kernels_irregular import gpu_list_fis_stats
+
+    n = 1 << 20
+    succ_d, head = device_gen_list(n, 42)
+    st = gpu_list_fis_stats(succ_d, head, 7, 32)
+    succ, head2 = ods.linked_list(n, 42)
+    assert head2 == head
+    _, (rounds, sizes, reduced, removed, subl) = olr.list_rank_with_stats(succ, head, 7)
+    assert (st.fis_rounds, st.round_sizes, st.reduced_size, st.removed_total, st.sublist_count) == (
+        rounds, sizes, reduced, removed, subl)

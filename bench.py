@@ -730,15 +730,16 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
 
     # end-to-end through the public API (host pinned buffers)
     wl.e2e_setup()
-    for _ in range(max(1, args.warmup)):
+    for _ in range(1):
         wl.e2e_step()
     torch.cuda.synchronize()
     barrier(world)
+    e_steps = max(1, min(args.steps, args.e2e_steps))
     e0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e_steps):
         wl.e2e_step()
     torch.cuda.synchronize()
-    e_s = (time.perf_counter() - e0) / args.steps
+    e_s = (time.perf_counter() - e0) / e_steps
     barrier(world)
     e_s = max_over_ranks(e_s, world)
 
@@ -770,7 +771,8 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
             "ms_per_step": e_s * 1e3,
-            "api": "public drop-in entry point on pinned host buffers",
+            "steps": e_steps,
+            "api": getattr(wl, "e2e_api", "public drop-in entry point on pinned host buffers"),
         },
         "clocks": clk,
         "config": wl.config(),
@@ -795,7 +797,8 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="hist", choices=sorted(WORKLOADS) + ["all"])
+    ap.add_argument("--workload", default="all", choices=sorted(WORKLOADS) + ["all"])
+    ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the end-to-end (host buffer) leg")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()

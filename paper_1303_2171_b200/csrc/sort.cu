@@ -22,6 +22,8 @@
 //   A digit position whose histogram has a single bucket is skipped (a stable
 //   pass over one bucket is the identity) — int64 keys below 2^32 sort in 4
 //   passes, a constant array in 0.
+#include <stdlib.h>
+
 #include <utility>
 
 #include "common.cuh"
@@ -89,123 +91,164 @@ __global__ void __launch_bounds__(512)
 }
 
 // ------------------------------------------------------------------ 2. onesweep pass
-template <typename K, bool HAS_V>
-__global__ void __launch_bounds__(SortCfg<K>::kThreads, 2)
+// T threads x I items per tile; RANK_MATCH selects __match_any_sync (one
+// MATCH per key row) instead of the eight-ballot multi-split.
+template <typename K, bool HAS_V, int T, int I, bool RANK_MATCH>
+__global__ void __launch_bounds__(T, 1024 / T)
     onesweep_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                     uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
                     const uint32_t* __restrict__ pass_hist, uint32_t* __restrict__ lookback,
                     uint32_t* __restrict__ tile_counter) {
-  constexpr int T = SortCfg<K>::kThreads, I = SortCfg<K>::kItems, W = T / 32, TILE = T * I;
+  constexpr int W = T / 32, TILE = T * I;
+  constexpr int DPT = 256 / T > 0 ? 256 / T : 1;  // digits per thread in digit-parallel phases
   __shared__ uint32_t s_whist[W][256];   // per-warp digit counters → exclusive warp offsets
   __shared__ uint32_t s_dstart[256];     // exclusive scan over digits of the tile counts
   __shared__ uint32_t s_goff[256];       // global offset of digit run minus its tile start
   __shared__ uint32_t s_gstart[256];     // global exclusive digit starts (this pass)
+  __shared__ uint32_t s_scr[8];
   __shared__ uint32_t s_tile;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   K* s_keys = reinterpret_cast<K*>(s_dyn);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + TILE);
+  static_assert(T >= 256 || DPT * T == 256, "digit phases need T | 256 or T >= 256");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int i = tid; i < W * 256; i += T) (&s_whist[0][0])[i] = 0;
-  // global digit starts: exclusive scan of this pass's histogram (warp 0..7: 32 digits each)
-  if (tid < 256) {
-    uint32_t h = pass_hist[tid];
-    uint32_t x = h;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    s_gstart[tid] = x - h;  // exclusive within the 32-digit group
-    if (lane == 31) s_dstart[warp] = x;  // group totals (scratch)
-  }
   __syncthreads();
-  if (tid < 256) {
-    uint32_t add = 0;
-    for (int g = 0; g < (tid >> 5); ++g) add += s_dstart[g];
-    s_gstart[tid] += add;
-  }
   const uint32_t tile = s_tile;
   const int64_t base = (int64_t)tile * TILE;
-  const int64_t wbase = base + (int64_t)warp * 32 * I;
+  const int valid = (int)min((int64_t)TILE, n - base);
+  const K* kt = kin + base;
+  const uint32_t* vt = HAS_V ? vin + base : nullptr;
+  const int wbase = warp * 32 * I;
 
+  // issue the tile's loads first; the global-start scan overlaps them
   K key[I];
   uint32_t val[I];
-  uint32_t rank[I];
 #pragma unroll
   for (int i = 0; i < I; ++i) {
-    const int64_t idx = wbase + i * 32 + lane;
-    const bool ok = idx < n;
-    key[i] = ok ? kin[idx] : (K)(~(K)0 ^ flip);  // padding sorts last (digit 255)
-    if (HAS_V) val[i] = ok ? vin[idx] : 0u;
+    const int idx = wbase + i * 32 + lane;
+    const bool ok = idx < valid;
+    key[i] = ok ? kt[idx] : (K)(~(K)0 ^ flip);  // padding sorts last (digit 255)
+    if (HAS_V) val[i] = ok ? vt[idx] : 0u;
   }
-  __syncthreads();  // s_whist zeroed, s_gstart ready
+  // global digit starts: exclusive scan of this pass's histogram
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const int d = tid + q * T;
+    if (d < 256) {
+      const uint32_t h = pass_hist[d];
+      uint32_t x = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      s_gstart[d] = x - h;
+      if (lane == 31) s_scr[d >> 5] = x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const int d = tid + q * T;
+    if (d < 256) {
+      uint32_t add = 0;
+      for (int g = 0; g < (d >> 5); ++g) add += s_scr[g];
+      s_gstart[d] += add;
+    }
+  }
 
-  // stable warp-level ranking: eight ballots find the lanes sharing a digit
+  // stable warp-level ranking of the I key rows
+  uint32_t dig[I], rank[I];
   uint32_t* wh = s_whist[warp];
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int i = 0; i < I; ++i) {
     const uint32_t d = digit_of<K>(key[i], flip, shift);
-    uint32_t peers = 0xffffffffu;
+    dig[i] = d;
+    uint32_t peers;
+    if (RANK_MATCH) {
+      peers = __match_any_sync(0xffffffffu, d);
+    } else {
+      peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      peers &= ((d >> b) & 1u) ? bal : ~bal;
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+      }
     }
     const uint32_t below = __popc(peers & lt);
     const uint32_t pre = wh[d];
     __syncwarp();
-    if (below == (uint32_t)__popc(peers) - 1u) wh[d] = pre + below + 1u;
+    if ((peers & ~(lt | (1u << lane))) == 0) wh[d] = pre + below + 1u;  // highest peer lane
     __syncwarp();
     rank[i] = pre + below;
   }
   __syncthreads();
 
   // per digit: exclusive offsets across warps, tile count, publish, look back
-  uint32_t cnt = 0;
-  if (tid < 256) {
-    for (int w = 0; w < W; ++w) {
-      const uint32_t t = s_whist[w][tid];
-      s_whist[w][tid] = cnt;
-      cnt += t;
-    }
-    if (tile == 0) st_relaxed(lookback + tid, kFlagInc | cnt);
-    else st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagAgg | cnt);
-    // exclusive scan of the tile counts over digits
-    uint32_t x = cnt;
+  uint32_t cnt[DPT], incl[DPT];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+  for (int q = 0; q < DPT; ++q) {
+    const int d = tid + q * T;
+    cnt[q] = 0;
+    if (d < 256) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint32_t t = s_whist[w][d];
+        s_whist[w][d] = c;
+        c += t;
+      }
+      cnt[q] = c;
+      if (tile == 0) st_relaxed(lookback + d, kFlagInc | c);
+      else st_relaxed(lookback + (size_t)tile * 256 + d, kFlagAgg | c);
+      uint32_t x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      incl[q] = x;
+      if (lane == 31) s_scr[d >> 5] = x;
     }
-    s_dstart[tid] = x - cnt;
-    s_goff[tid] = x;  // scratch: inclusive within group
   }
   __syncthreads();
-  uint32_t dstart = 0, excl = 0;
-  if (tid < 256) {
-    uint32_t add = 0;
-    for (int g = 0; g < (tid >> 5); ++g) add += s_goff[g * 32 + 31];
-    dstart = s_dstart[tid] + add;
-    if (tile > 0) {
-      int64_t t = (int64_t)tile - 1;
-      while (true) {
-        const uint32_t w = ld_relaxed(lookback + (size_t)t * 256 + tid);
-        const uint32_t flag = w & ~kCountMask;
-        if (flag == 0) continue;  // predecessor still ranking: spin
-        excl += w & kCountMask;
-        if (flag == kFlagInc) break;
-        --t;
+  uint32_t dstart[DPT], excl[DPT];
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const int d = tid + q * T;
+    dstart[q] = 0;
+    excl[q] = 0;
+    if (d < 256) {
+      uint32_t add = 0;
+      for (int g = 0; g < (d >> 5); ++g) add += s_scr[g];
+      dstart[q] = incl[q] - cnt[q] + add;
+      if (tile > 0) {
+        int64_t t = (int64_t)tile - 1;
+        uint32_t e = 0;
+        while (true) {
+          const uint32_t w = ld_relaxed(lookback + (size_t)t * 256 + d);
+          const uint32_t flag = w & ~kCountMask;
+          if (flag == 0) continue;  // predecessor still ranking: spin
+          e += w & kCountMask;
+          if (flag == kFlagInc) break;
+          --t;
+        }
+        st_relaxed(lookback + (size_t)tile * 256 + d, kFlagInc | (e + cnt[q]));
+        excl[q] = e;
       }
-      st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagInc | (excl + cnt));
     }
   }
-  __syncthreads();  // every thread has read the scan scratch
-  if (tid < 256) {
-    s_dstart[tid] = dstart;
-    s_goff[tid] = s_gstart[tid] + excl - dstart;
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const int d = tid + q * T;
+    if (d < 256) {
+      s_dstart[d] = dstart[q];
+      s_goff[d] = s_gstart[d] + excl[q] - dstart[q];
+    }
   }
   __syncthreads();
 
@@ -213,8 +256,7 @@ __global__ void __launch_bounds__(SortCfg<K>::kThreads, 2)
   uint32_t pos[I];
 #pragma unroll
   for (int i = 0; i < I; ++i) {
-    const uint32_t d = digit_of<K>(key[i], flip, shift);
-    pos[i] = s_dstart[d] + s_whist[warp][d] + rank[i];
+    pos[i] = s_dstart[dig[i]] + s_whist[warp][dig[i]] + rank[i];
     s_keys[pos[i]] = key[i];
   }
   if (HAS_V) {
@@ -222,7 +264,6 @@ __global__ void __launch_bounds__(SortCfg<K>::kThreads, 2)
     for (int i = 0; i < I; ++i) s_vals[pos[i]] = val[i];
   }
   __syncthreads();
-  const int valid = (int)min((int64_t)TILE, n - base);
   for (int j = tid; j < valid; j += T) {
     const K k = s_keys[j];
     const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
@@ -231,16 +272,65 @@ __global__ void __launch_bounds__(SortCfg<K>::kThreads, 2)
   }
 }
 
-template <typename K>
+template <typename K, int T, int I>
 size_t onesweep_smem(bool has_v) {
-  constexpr int TILE = SortCfg<K>::kThreads * SortCfg<K>::kItems;
-  return (size_t)TILE * sizeof(K) + (has_v ? (size_t)TILE * 4 : 0);
+  return (size_t)T * I * sizeof(K) + (has_v ? (size_t)T * I * 4 : 0);
+}
+
+// Tuning variants (selected by HB_SORT_CFG for experiments; default = best measured)
+struct PassArgs {
+  const void* kin; void* kout; const uint32_t* vin; uint32_t* vout;
+  int64_t n; int shift; uint64_t flip; const uint32_t* hist; uint32_t* lookback; uint32_t* counter;
+};
+
+template <typename K, int T, int I, bool M>
+int launch_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  const size_t smem = onesweep_smem<K, T, I>(a.vin != nullptr);
+  if (a.vin) {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_kernel<K, true, T, I, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_kernel<K, true, T, I, M><<<(unsigned)tiles, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.hist, a.lookback, a.counter);
+  } else {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_kernel<K, false, T, I, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_kernel<K, false, T, I, M><<<(unsigned)tiles, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.hist, a.lookback, a.counter);
+  }
+  return check_launch();
+}
+
+int sort_variant() {
+  static int v = [] {
+    const char* e = getenv("HB_SORT_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <typename K>
+int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
+  if constexpr (sizeof(K) == 8) {
+    switch (sort_variant()) {
+      case 1: return launch_pass<K, 512, 8, false>(a, s, tiles, dry);
+      default: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
+    }
+  } else {
+  switch (sort_variant()) {
+    case 1: return launch_pass<K, 512, 12, false>(a, s, tiles, dry);
+    case 2: return launch_pass<K, 512, 12, true>(a, s, tiles, dry);
+    case 3: return launch_pass<K, 256, 12, false>(a, s, tiles, dry);
+    case 4: return launch_pass<K, 256, 16, true>(a, s, tiles, dry);
+    case 5: return launch_pass<K, 384, 16, true>(a, s, tiles, dry);
+    default: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
+  }
+  }
 }
 
 template <typename K>
 int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cudaStream_t s) {
   constexpr int P = SortCfg<K>::kPasses;
-  constexpr int TILE = SortCfg<K>::kThreads * SortCfg<K>::kItems;
   DeviceInfo di;
   HB_TRY(device_info(&di));
   if (passes_done) *passes_done = 0;
@@ -249,7 +339,6 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
     set_error("radix sort supports n < 2^30 keys per call (got %lld)", (long long)n);
     return HB_EINVAL;
   }
-  const int64_t tiles = ceil_div(n, TILE);
   DevBuf hist, kalt, valt, lb;
   HB_TRY(alloc(&hist, (size_t)P * 256 * 4, s));
   HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, (size_t)P * 256 * 4, s));
@@ -273,14 +362,12 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
 
   HB_TRY(alloc(&kalt, (size_t)n * sizeof(K), s));
   if (vals) HB_TRY(alloc(&valt, (size_t)n * 4, s));
+  int64_t tiles = 0;
+  PassArgs pa{};
+  pa.n = n;
+  HB_TRY(run_pass<K>(pa, s, &tiles, true));
   const size_t lb_words = (size_t)tiles * 256 + 32;  // + tile counter (padded)
   HB_TRY(alloc(&lb, lb_words * 4, s));
-  const size_t smem = onesweep_smem<K>(vals != nullptr);
-  if (vals) {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  } else {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  }
   K* kcur = keys;
   K* knext = kalt.as<K>();
   uint32_t* vcur = vals;
@@ -289,15 +376,10 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
   for (int p = 0; p < P; ++p) {
     if (!live[p]) continue;
     HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
-    const uint32_t* ph = hist.as<uint32_t>() + p * 256;
-    if (vals) {
-      onesweep_kernel<K, true><<<(unsigned)tiles, SortCfg<K>::kThreads, smem, s>>>(
-          kcur, knext, vcur, vnext, n, 8 * p, flip, ph, lb.as<uint32_t>(), counter);
-    } else {
-      onesweep_kernel<K, false><<<(unsigned)tiles, SortCfg<K>::kThreads, smem, s>>>(
-          kcur, knext, nullptr, nullptr, n, 8 * p, flip, ph, lb.as<uint32_t>(), counter);
-    }
-    HB_TRY(check_launch());
+    pa.kin = kcur; pa.kout = knext; pa.vin = vcur; pa.vout = vals ? vnext : nullptr;
+    pa.shift = 8 * p; pa.flip = (uint64_t)flip; pa.hist = hist.as<uint32_t>() + p * 256;
+    pa.lookback = lb.as<uint32_t>(); pa.counter = counter;
+    HB_TRY(run_pass<K>(pa, s, &tiles, false));
     std::swap(kcur, knext);
     std::swap(vcur, vnext);
   }

@@ -272,6 +272,213 @@ __global__ void __launch_bounds__(T, 1024 / T)
   }
 }
 
+// ------------------------------------------------------------------ 2b. persistent onesweep
+// Same pass as onesweep_kernel, but each CTA stays resident and loops over
+// tiles: while tile a_i is ranked / looked back / scattered, the tile a_{i+1}
+// (id taken one iteration earlier) is already streaming into the other
+// shared-memory stage with cp.async, and the id of a_{i+2} is being fetched.
+// Dependencies only point to smaller tile ids and every CTA handles its tiles
+// in increasing order, so the smallest unfinished tile always progresses.
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// stage a tile's keys/vals (valid elements only) into smem; 16-byte copies when aligned
+template <typename K, bool HAS_V, int T, int I>
+__device__ __forceinline__ void stage_tile(K* sk, uint32_t* sv, const K* kin, const uint32_t* vin,
+                                           int64_t base, int valid, bool vec_ok) {
+  constexpr int TILE = T * I;
+  const int tid = threadIdx.x;
+  if (vec_ok) {
+    constexpr int KV = 16 / sizeof(K);
+    const int kvec = valid / KV;
+    for (int v = tid; v < kvec; v += T) cp_async16(sk + v * KV, kin + base + v * KV);
+    for (int e = kvec * KV + tid; e < valid; e += T) {
+      if constexpr (sizeof(K) == 4) cp_async4(sk + e, kin + base + e);
+      else { cp_async4(reinterpret_cast<uint32_t*>(sk + e), reinterpret_cast<const uint32_t*>(kin + base + e));
+             cp_async4(reinterpret_cast<uint32_t*>(sk + e) + 1, reinterpret_cast<const uint32_t*>(kin + base + e) + 1); }
+    }
+    if (HAS_V) {
+      const int vvec = valid / 4;
+      for (int v = tid; v < vvec; v += T) cp_async16(sv + v * 4, vin + base + v * 4);
+      for (int e = vvec * 4 + tid; e < valid; e += T) cp_async4(sv + e, vin + base + e);
+    }
+  } else {
+    for (int e = tid; e < valid; e += T) {
+      if constexpr (sizeof(K) == 4) cp_async4(sk + e, kin + base + e);
+      else { cp_async4(reinterpret_cast<uint32_t*>(sk + e), reinterpret_cast<const uint32_t*>(kin + base + e));
+             cp_async4(reinterpret_cast<uint32_t*>(sk + e) + 1, reinterpret_cast<const uint32_t*>(kin + base + e) + 1); }
+      if (HAS_V) cp_async4(sv + e, vin + base + e);
+    }
+  }
+  (void)TILE;
+  cp_async_commit();
+}
+
+template <typename K, bool HAS_V, int T, int I>
+__global__ void __launch_bounds__(T, 3)
+    onesweep_persist_kernel(const K* __restrict__ kin, K* __restrict__ kout,
+                            const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout, int64_t n,
+                            int shift, K flip, const uint32_t* __restrict__ pass_hist,
+                            uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter,
+                            int64_t ntiles, int vec_ok) {
+  constexpr int W = T / 32, TILE = T * I;
+  static_assert(T == 256, "digit-parallel phases assume one digit per thread");
+  __shared__ uint32_t s_whist[W][256];
+  __shared__ uint32_t s_dstart[256];
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_gstart[256];
+  __shared__ uint32_t s_scr[8];
+  __shared__ uint32_t s_next[2];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  constexpr size_t STAGE = (size_t)TILE * sizeof(K) + (HAS_V ? (size_t)TILE * 4 : 0);
+  auto stage_k = [&](int st) { return reinterpret_cast<K*>(s_dyn + st * STAGE); };
+  auto stage_v = [&](int st) { return reinterpret_cast<uint32_t*>(s_dyn + st * STAGE + (size_t)TILE * sizeof(K)); };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // global digit starts (once per CTA)
+  {
+    const uint32_t h = pass_hist[tid];
+    uint32_t x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_gstart[tid] = x - h;
+    if (lane == 31) s_scr[warp] = x;
+    __syncthreads();
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    s_gstart[tid] += add;
+  }
+  if (tid == 0) {
+    s_next[0] = atomicAdd(tile_counter, 1u);
+    s_next[1] = atomicAdd(tile_counter, 1u);
+  }
+  __syncthreads();
+  uint32_t tile = s_next[0];
+  uint32_t nxt = s_next[1];
+  if (tile < ntiles) {
+    const int64_t b0 = (int64_t)tile * TILE;
+    stage_tile<K, HAS_V, T, I>(stage_k(0), stage_v(0), kin, vin, b0, (int)min((int64_t)TILE, n - b0), vec_ok);
+  }
+  int st = 0;
+  const uint32_t lt = lanemask_lt();
+  while (tile < ntiles) {
+    const int64_t base = (int64_t)tile * TILE;
+    const int valid = (int)min((int64_t)TILE, n - base);
+    for (int i = tid; i < W * 256; i += T) (&s_whist[0][0])[i] = 0;
+    cp_async_wait_all();
+    __syncthreads();  // stage st landed; s_whist zeroed; s_next consumed
+    // prefetch the next tile into the other stage and fetch the id after it
+    if (nxt < ntiles) {
+      const int64_t b1 = (int64_t)nxt * TILE;
+      stage_tile<K, HAS_V, T, I>(stage_k(st ^ 1), stage_v(st ^ 1), kin, vin, b1,
+                                 (int)min((int64_t)TILE, n - b1), vec_ok);
+    }
+    if (tid == 0) s_next[0] = atomicAdd(tile_counter, 1u);
+
+    K* sk = stage_k(st);
+    uint32_t* sv = stage_v(st);
+    const int wbase = warp * 32 * I;
+    K key[I];
+    uint32_t val[I], dig[I], rank[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const int idx = wbase + i * 32 + lane;
+      const bool ok = idx < valid;
+      key[i] = ok ? sk[idx] : (K)(~(K)0 ^ flip);
+      if (HAS_V) val[i] = ok ? sv[idx] : 0u;
+    }
+    uint32_t* wh = s_whist[warp];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const uint32_t d = digit_of<K>(key[i], flip, shift);
+      dig[i] = d;
+      uint32_t peers = 0xffffffffu;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+      }
+      const uint32_t below = __popc(peers & lt);
+      const uint32_t pre = wh[d];
+      __syncwarp();
+      if ((peers & ~(lt | (1u << lane))) == 0) wh[d] = pre + below + 1u;
+      __syncwarp();
+      rank[i] = pre + below;
+    }
+    __syncthreads();  // all keys read from stage st (it becomes the re-order buffer)
+
+    // digit tid: warp offsets, tile count, publish, scan, look back
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t t = s_whist[w][tid];
+      s_whist[w][tid] = c;
+      c += t;
+    }
+    if (tile == 0) st_relaxed(lookback + tid, kFlagInc | c);
+    else st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagAgg | c);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_scr[warp] = x;
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint32_t w = ld_relaxed(lookback + (size_t)t * 256 + tid);
+        const uint32_t flag = w & ~kCountMask;
+        if (flag == 0) continue;
+        excl += w & kCountMask;
+        if (flag == kFlagInc) break;
+        --t;
+      }
+      st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagInc | (excl + c));
+    }
+    __syncthreads();
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    const uint32_t dstart = x - c + add;
+    s_dstart[tid] = dstart;
+    s_goff[tid] = s_gstart[tid] + excl - dstart;
+    const uint32_t after = s_next[0];  // id of the tile after the prefetched one
+    __syncthreads();
+
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const uint32_t p = s_dstart[dig[i]] + s_whist[warp][dig[i]] + rank[i];
+      sk[p] = key[i];
+      if (HAS_V) sv[p] = val[i];
+    }
+    __syncthreads();
+    for (int j = tid; j < valid; j += T) {
+      const K k = sk[j];
+      const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
+      kout[dst] = k;
+      if (HAS_V) vout[dst] = sv[j];
+    }
+    // rotate: the prefetched tile becomes current (the loop-top barrier
+    // orders this stage's scatter before it is refilled)
+    tile = nxt;
+    nxt = after;
+    st ^= 1;
+  }
+  cp_async_wait_all();
+}
+
 template <typename K, int T, int I>
 size_t onesweep_smem(bool has_v) {
   return (size_t)T * I * sizeof(K) + (has_v ? (size_t)T * I * 4 : 0);
@@ -309,11 +516,37 @@ int sort_variant() {
   return v;
 }
 
+template <typename K, int T, int I>
+int launch_persist(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  const bool hv = a.vin != nullptr;
+  const size_t stage = (size_t)T * I * sizeof(K) + (hv ? (size_t)T * I * 4 : 0);
+  const size_t smem = 2 * stage;
+  const int vec_ok = ((uintptr_t)a.kin % 16 == 0) && (!hv || (uintptr_t)a.vin % 16 == 0);
+  int64_t grid = (int64_t)di.sms * 3;
+  if (grid > tiles) grid = tiles;
+  if (hv) {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_persist_kernel<K, true, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_persist_kernel<K, true, T, I><<<(unsigned)grid, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.hist, a.lookback, a.counter, tiles, vec_ok);
+  } else {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_persist_kernel<K, false, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_persist_kernel<K, false, T, I><<<(unsigned)grid, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.hist, a.lookback, a.counter, tiles, vec_ok);
+  }
+  return check_launch();
+}
+
 template <typename K>
 int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
   if constexpr (sizeof(K) == 8) {
     switch (sort_variant()) {
       case 1: return launch_pass<K, 512, 8, false>(a, s, tiles, dry);
+      case 6: return launch_persist<K, 256, 8>(a, s, tiles, dry);
       default: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
     }
   } else {
@@ -323,6 +556,8 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 3: return launch_pass<K, 256, 12, false>(a, s, tiles, dry);
     case 4: return launch_pass<K, 256, 16, true>(a, s, tiles, dry);
     case 5: return launch_pass<K, 384, 16, true>(a, s, tiles, dry);
+    case 6: return launch_persist<K, 256, 12>(a, s, tiles, dry);
+    case 7: return launch_persist<K, 256, 16>(a, s, tiles, dry);
     default: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
   }
   }

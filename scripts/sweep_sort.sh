@@ -1,1 +1,1 @@
-for c in 0 1 2 3 4 5; do HB_SORT_CFG=$c python scripts/sweep_sort.py run; done
+for c in ${CFGS:-1 6 7}; do HB_SORT_CFG=$c python scripts/sweep_sort.py run; done

@@ -479,6 +479,203 @@ __global__ void __launch_bounds__(T, 3)
   cp_async_wait_all();
 }
 
+// ------------------------------------------------------------------ 2c. persistent onesweep, TMA bulk prefetch
+// One elected thread per CTA takes the next tile id and streams that tile's
+// keys/payload into the other shared-memory stage with cp.async.bulk
+// (completion on an mbarrier, expect_tx bytes) while all warps work on the
+// current tile.  Tile ids are taken when a tile starts (never two ahead), so
+// a tile's predecessors are always current tiles of other CTAs.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(a), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* smem, const void* g, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(g), "r"(bytes), "r"(b) : "memory");
+}
+
+template <typename K, bool HAS_V, int T, int I>
+__device__ __forceinline__ void tma_stage(K* sk, uint32_t* sv, const K* kin, const uint32_t* vin,
+                                          int64_t base, int valid, uint64_t* bar) {
+  const uint32_t kb = (uint32_t)(valid * sizeof(K)) & ~15u;
+  const uint32_t vb = HAS_V ? ((uint32_t)(valid * 4) & ~15u) : 0u;
+  mbar_expect_tx(bar, kb + vb);
+  if (kb) tma_bulk_g2s(sk, kin + base, kb, bar);
+  if (vb) tma_bulk_g2s(sv, vin + base, vb, bar);
+}
+
+template <typename K, bool HAS_V, int T, int I>
+__global__ void __launch_bounds__(T, 3)
+    onesweep_tma_kernel(const K* __restrict__ kin, K* __restrict__ kout,
+                        const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout, int64_t n,
+                        int shift, K flip, const uint32_t* __restrict__ pass_hist,
+                        uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter,
+                        int64_t ntiles) {
+  constexpr int W = T / 32, TILE = T * I;
+  static_assert(T == 256, "digit-parallel phases assume one digit per thread");
+  __shared__ uint32_t s_whist[W][256];
+  __shared__ uint32_t s_dstart[256];
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_gstart[256];
+  __shared__ uint32_t s_scr[8];
+  __shared__ uint32_t s_next;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  constexpr size_t STAGE = (size_t)TILE * sizeof(K) + (HAS_V ? (size_t)TILE * 4 : 0);
+  auto stage_k = [&](int st) { return reinterpret_cast<K*>(s_dyn + st * STAGE); };
+  auto stage_v = [&](int st) { return reinterpret_cast<uint32_t*>(s_dyn + st * STAGE + (size_t)TILE * sizeof(K)); };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t t0 = atomicAdd(tile_counter, 1u);
+    s_next = t0;
+    if (t0 < ntiles) {
+      const int64_t b0 = (int64_t)t0 * TILE;
+      tma_stage<K, HAS_V, T, I>(stage_k(0), stage_v(0), kin, vin, b0, (int)min((int64_t)TILE, n - b0), &s_bar[0]);
+    }
+  }
+  {  // global digit starts (once per CTA)
+    const uint32_t h = pass_hist[tid];
+    uint32_t x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_gstart[tid] = x - h;
+    if (lane == 31) s_scr[warp] = x;
+    __syncthreads();
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    s_gstart[tid] += add;
+  }
+  uint32_t tile = s_next;
+  uint32_t phase[2] = {0u, 0u};
+  int st = 0;
+  const uint32_t lt = lanemask_lt();
+  while (tile < ntiles) {
+    const int64_t base = (int64_t)tile * TILE;
+    const int valid = (int)min((int64_t)TILE, n - base);
+    for (int i = tid; i < W * 256; i += T) (&s_whist[0][0])[i] = 0;
+    mbar_wait(&s_bar[st], phase[st]);
+    phase[st] ^= 1u;
+    __syncthreads();  // stage st landed; s_whist zeroed; previous stage fully consumed
+    if (tid == 0) {  // next tile: id + bulk prefetch into the other stage
+      const uint32_t nt = atomicAdd(tile_counter, 1u);
+      s_next = nt;
+      if (nt < ntiles) {
+        const int64_t b1 = (int64_t)nt * TILE;
+        tma_stage<K, HAS_V, T, I>(stage_k(st ^ 1), stage_v(st ^ 1), kin, vin, b1,
+                                  (int)min((int64_t)TILE, n - b1), &s_bar[st ^ 1]);
+      }
+    }
+    K* sk = stage_k(st);
+    uint32_t* sv = stage_v(st);
+    const int kvec = (int)(((uint32_t)(valid * sizeof(K)) & ~15u) / sizeof(K));
+    const int vvec = (int)(((uint32_t)(valid * 4) & ~15u) / 4);
+    const int wbase = warp * 32 * I;
+    K key[I];
+    uint32_t val[I], dig[I], rank[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const int idx = wbase + i * 32 + lane;
+      key[i] = idx < kvec ? sk[idx] : (idx < valid ? kin[base + idx] : (K)(~(K)0 ^ flip));
+      if (HAS_V) val[i] = idx < vvec ? sv[idx] : (idx < valid ? vin[base + idx] : 0u);
+    }
+    uint32_t* wh = s_whist[warp];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const uint32_t d = digit_of<K>(key[i], flip, shift);
+      dig[i] = d;
+      uint32_t peers = 0xffffffffu;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+      }
+      const uint32_t below = __popc(peers & lt);
+      const uint32_t pre = wh[d];
+      __syncwarp();
+      if ((peers & ~(lt | (1u << lane))) == 0) wh[d] = pre + below + 1u;
+      __syncwarp();
+      rank[i] = pre + below;
+    }
+    __syncthreads();
+
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t t = s_whist[w][tid];
+      s_whist[w][tid] = c;
+      c += t;
+    }
+    if (tile == 0) st_relaxed(lookback + tid, kFlagInc | c);
+    else st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagAgg | c);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_scr[warp] = x;
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint32_t w = ld_relaxed(lookback + (size_t)t * 256 + tid);
+        const uint32_t flag = w & ~kCountMask;
+        if (flag == 0) continue;
+        excl += w & kCountMask;
+        if (flag == kFlagInc) break;
+        --t;
+      }
+      st_relaxed(lookback + (size_t)tile * 256 + tid, kFlagInc | (excl + c));
+    }
+    __syncthreads();
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    const uint32_t dstart = x - c + add;
+    s_dstart[tid] = dstart;
+    s_goff[tid] = s_gstart[tid] + excl - dstart;
+    __syncthreads();
+
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const uint32_t p = s_dstart[dig[i]] + s_whist[warp][dig[i]] + rank[i];
+      sk[p] = key[i];
+      if (HAS_V) sv[p] = val[i];
+    }
+    __syncthreads();
+    for (int j = tid; j < valid; j += T) {
+      const K k = sk[j];
+      const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
+      kout[dst] = k;
+      if (HAS_V) vout[dst] = sv[j];
+    }
+    // order this stage's generic-proxy accesses before the bulk copy that
+    // will refill it (issued after the next loop-top barrier)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tile = s_next;
+    st ^= 1;
+  }
+}
+
 template <typename K, int T, int I>
 size_t onesweep_smem(bool has_v) {
   return (size_t)T * I * sizeof(K) + (has_v ? (size_t)T * I * 4 : 0);
@@ -541,12 +738,39 @@ int launch_persist(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool d
   return check_launch();
 }
 
+template <typename K, int T, int I>
+int launch_tma(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  const bool hv = a.vin != nullptr;
+  if ((uintptr_t)a.kin % 16 || (hv && (uintptr_t)a.vin % 16))  // bulk copies need 16-byte alignment
+    return launch_pass<K, 512, (sizeof(K) == 4 ? 12 : 8), false>(a, s, tiles_out, dry);
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  const size_t stage = (size_t)T * I * sizeof(K) + (hv ? (size_t)T * I * 4 : 0);
+  const size_t smem = 2 * stage;
+  int64_t grid = (int64_t)di.sms * 3;
+  if (grid > tiles) grid = tiles;
+  if (hv) {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_tma_kernel<K, true, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_tma_kernel<K, true, T, I><<<(unsigned)grid, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.hist, a.lookback, a.counter, tiles);
+  } else {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_tma_kernel<K, false, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_tma_kernel<K, false, T, I><<<(unsigned)grid, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.hist, a.lookback, a.counter, tiles);
+  }
+  return check_launch();
+}
+
 template <typename K>
 int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
   if constexpr (sizeof(K) == 8) {
     switch (sort_variant()) {
       case 1: return launch_pass<K, 512, 8, false>(a, s, tiles, dry);
       case 6: return launch_persist<K, 256, 8>(a, s, tiles, dry);
+      case 8: return launch_tma<K, 256, 8>(a, s, tiles, dry);
       default: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
     }
   } else {
@@ -558,6 +782,8 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 5: return launch_pass<K, 384, 16, true>(a, s, tiles, dry);
     case 6: return launch_persist<K, 256, 12>(a, s, tiles, dry);
     case 7: return launch_persist<K, 256, 16>(a, s, tiles, dry);
+    case 8: return launch_tma<K, 256, 12>(a, s, tiles, dry);
+    case 9: return launch_tma<K, 256, 16>(a, s, tiles, dry);
     default: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
   }
   }

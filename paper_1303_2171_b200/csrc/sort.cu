@@ -676,6 +676,166 @@ __global__ void __launch_bounds__(T, 3)
   }
 }
 
+// ------------------------------------------------------------------ 2d. onesweep with early counts
+// Critical-path restructuring of onesweep_kernel (CUB calls the idea "early
+// counts"): the tile's digit counts come from per-warp shared-memory atomics
+// right after the load, so the AGGREGATE is published before the ranking;
+// warps 0-7 (one digit per thread) then run the look-back while warps 8-15
+// already rank their keys; warps 0-7 rank after.  Ranks are warp-local
+// (stable ballot multi-split); final positions = per-(warp, digit) base +
+// rank.  Global digit starts come pre-scanned (scan_hist_kernel).
+__global__ void scan_hist_kernel(const uint32_t* __restrict__ hist, uint32_t* __restrict__ gstart, int passes) {
+  const int p = blockIdx.x;
+  if (p >= passes) return;
+  __shared__ uint32_t scr[8];
+  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  const uint32_t h = hist[p * 256 + d];
+  uint32_t x = h;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scr[warp] = x;
+  __syncthreads();
+  uint32_t add = 0;
+  for (int g = 0; g < warp; ++g) add += scr[g];
+  gstart[p * 256 + d] = x - h + add;
+}
+
+__device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <typename K, bool HAS_V, int I>
+__global__ void __launch_bounds__(512, 2)
+    onesweep_ec_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
+                       uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
+                       const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
+                       uint32_t* __restrict__ tile_counter) {
+  constexpr int T = 512, W = T / 32, TILE = T * I;
+  __shared__ uint32_t s_base[W][256];   // per-warp counts → per-(warp, digit) tile positions
+  __shared__ uint32_t s_run[W][256];    // warp-local running counts for the stable ranking
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_scr[8];
+  __shared__ uint32_t s_tile;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  K* s_keys = reinterpret_cast<K*>(s_dyn);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + TILE);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < W * 256; i += T) {
+    (&s_base[0][0])[i] = 0;
+    (&s_run[0][0])[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * TILE;
+  const int valid = (int)min((int64_t)TILE, n - base);
+  const K* kt = kin + base;
+  const uint32_t* vt = HAS_V ? vin + base : nullptr;
+  const int wbase = warp * 32 * I;
+  K key[I];
+  uint32_t val[I], dig[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const int idx = wbase + i * 32 + lane;
+    const bool ok = idx < valid;
+    key[i] = ok ? kt[idx] : (K)(~(K)0 ^ flip);
+    if (HAS_V) val[i] = ok ? vt[idx] : 0u;
+  }
+  uint32_t gs = 0;
+  if (tid < 256) gs = gstart[tid];
+  // early per-warp digit counts
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    dig[i] = digit_of<K>(key[i], flip, shift);
+    atomicAdd(&s_base[warp][dig[i]], 1u);
+  }
+  __syncthreads();
+
+  uint32_t rank[I];
+  const uint32_t lt = lanemask_lt();
+  auto rank_keys = [&]() {
+    uint32_t* wr = s_run[warp];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const uint32_t d = dig[i];
+      uint32_t peers = 0xffffffffu;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+      }
+      const uint32_t below = __popc(peers & lt);
+      const uint32_t pre = wr[d];
+      __syncwarp();
+      if ((peers & ~(lt | (1u << lane))) == 0) wr[d] = pre + below + 1u;
+      __syncwarp();
+      rank[i] = pre + below;
+    }
+  };
+
+  if (tid >= 256) {
+    rank_keys();  // warps 8-15 rank while warps 0-7 publish and look back
+  } else {
+    const int d = tid;
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) c += s_base[w][d];
+    if (tile == 0) st_relaxed(lookback + d, kFlagInc | c);
+    else st_relaxed(lookback + (size_t)tile * 256 + d, kFlagAgg | c);
+    // exclusive scan over digits (256 threads, named barrier 1)
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_scr[warp] = x;
+    bar_named(1, 256);
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    const uint32_t dstart = x - c + add;
+    uint32_t run = dstart;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t t = s_base[w][d];
+      s_base[w][d] = run;
+      run += t;
+    }
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint32_t wv = ld_relaxed(lookback + (size_t)t * 256 + d);
+        const uint32_t flag = wv & ~kCountMask;
+        if (flag == 0) continue;
+        excl += wv & kCountMask;
+        if (flag == kFlagInc) break;
+        --t;
+      }
+      st_relaxed(lookback + (size_t)tile * 256 + d, kFlagInc | (excl + c));
+    }
+    s_goff[d] = gs + excl - dstart;
+    rank_keys();
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const uint32_t p = s_base[warp][dig[i]] + rank[i];
+    s_keys[p] = key[i];
+    if (HAS_V) s_vals[p] = val[i];
+  }
+  __syncthreads();
+  for (int j = tid; j < valid; j += T) {
+    const K k = s_keys[j];
+    const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
+    kout[dst] = k;
+    if (HAS_V) vout[dst] = s_vals[j];
+  }
+}
+
 template <typename K, int T, int I>
 size_t onesweep_smem(bool has_v) {
   return (size_t)T * I * sizeof(K) + (has_v ? (size_t)T * I * 4 : 0);
@@ -685,7 +845,26 @@ size_t onesweep_smem(bool has_v) {
 struct PassArgs {
   const void* kin; void* kout; const uint32_t* vin; uint32_t* vout;
   int64_t n; int shift; uint64_t flip; const uint32_t* hist; uint32_t* lookback; uint32_t* counter;
+  const uint32_t* gstart;  // pre-scanned digit starts of this pass
 };
+
+template <typename K, int I>
+int launch_ec(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)512 * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  const size_t smem = (size_t)512 * I * sizeof(K) + (a.vin ? (size_t)512 * I * 4 : 0);
+  if (a.vin) {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, true, I><<<(unsigned)tiles, 512, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
+  } else {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, false, I><<<(unsigned)tiles, 512, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
+  }
+  return check_launch();
+}
 
 template <typename K, int T, int I, bool M>
 int launch_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
@@ -771,6 +950,7 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
       case 1: return launch_pass<K, 512, 8, false>(a, s, tiles, dry);
       case 6: return launch_persist<K, 256, 8>(a, s, tiles, dry);
       case 8: return launch_tma<K, 256, 8>(a, s, tiles, dry);
+      case 10: return launch_ec<K, 8>(a, s, tiles, dry);
       default: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
     }
   } else {
@@ -784,6 +964,8 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 7: return launch_persist<K, 256, 16>(a, s, tiles, dry);
     case 8: return launch_tma<K, 256, 12>(a, s, tiles, dry);
     case 9: return launch_tma<K, 256, 16>(a, s, tiles, dry);
+    case 10: return launch_ec<K, 12>(a, s, tiles, dry);
+    case 11: return launch_ec<K, 8>(a, s, tiles, dry);
     default: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
   }
   }
@@ -821,6 +1003,10 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
   if (passes_done) *passes_done = nlive;
   if (nlive == 0) return HB_OK;
 
+  DevBuf gst;
+  HB_TRY(alloc(&gst, (size_t)P * 256 * 4, s));
+  scan_hist_kernel<<<P, 256, 0, s>>>(hist.as<uint32_t>(), gst.as<uint32_t>(), P);
+  HB_TRY(check_launch());
   HB_TRY(alloc(&kalt, (size_t)n * sizeof(K), s));
   if (vals) HB_TRY(alloc(&valt, (size_t)n * 4, s));
   int64_t tiles = 0;
@@ -839,7 +1025,7 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
     HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
     pa.kin = kcur; pa.kout = knext; pa.vin = vcur; pa.vout = vals ? vnext : nullptr;
     pa.shift = 8 * p; pa.flip = (uint64_t)flip; pa.hist = hist.as<uint32_t>() + p * 256;
-    pa.lookback = lb.as<uint32_t>(); pa.counter = counter;
+    pa.lookback = lb.as<uint32_t>(); pa.counter = counter; pa.gstart = gst.as<uint32_t>() + p * 256;
     HB_TRY(run_pass<K>(pa, s, &tiles, false));
     std::swap(kcur, knext);
     std::swap(vcur, vnext);

@@ -60,6 +60,25 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Lanes of the warp holding the same 8-bit digit: peers &= ~(ballot_b ^ m_b),
+// m_b = all-ones when bit b of my digit is set — four instructions per bit
+// (LOP3 → predicate, VOTE, SELP, LOP3 0x90).
+__device__ __forceinline__ uint32_t match_digit8(uint32_t d) {
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal, m;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
+        "selp.b32 m, 0xffffffff, 0, p;\n\t"
+        "lop3.b32 %0, %0, bal, m, 0x90;\n\t}"
+        : "+r"(peers)
+        : "r"(d), "r"(1u << b));
+  }
+  return peers;
+}
+
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, K flip, int shift) {
   return (uint32_t)((key ^ flip) >> shift) & 255u;
@@ -760,12 +779,7 @@ __global__ void __launch_bounds__(512, 2)
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       const uint32_t d = dig[i];
-      uint32_t peers = 0xffffffffu;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bal : ~bal;
-      }
+      const uint32_t peers = match_digit8(d);
       const uint32_t below = __popc(peers & lt);
       const uint32_t pre = wr[d];
       __syncwarp();

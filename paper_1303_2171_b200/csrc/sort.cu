@@ -187,17 +187,7 @@ __global__ void __launch_bounds__(T, 1024 / T)
   for (int i = 0; i < I; ++i) {
     const uint32_t d = digit_of<K>(key[i], flip, shift);
     dig[i] = d;
-    uint32_t peers;
-    if (RANK_MATCH) {
-      peers = __match_any_sync(0xffffffffu, d);
-    } else {
-      peers = 0xffffffffu;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bal : ~bal;
-      }
-    }
+    const uint32_t peers = RANK_MATCH ? __match_any_sync(0xffffffffu, d) : match_digit8(d);
     const uint32_t below = __popc(peers & lt);
     const uint32_t pre = wh[d];
     __syncwarp();
@@ -964,8 +954,8 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
       case 1: return launch_pass<K, 512, 8, false>(a, s, tiles, dry);
       case 6: return launch_persist<K, 256, 8>(a, s, tiles, dry);
       case 8: return launch_tma<K, 256, 8>(a, s, tiles, dry);
-      case 10: return launch_ec<K, 8>(a, s, tiles, dry);
-      default: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
+      case 12: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
+      default: return launch_ec<K, 8>(a, s, tiles, dry);
     }
   } else {
   switch (sort_variant()) {
@@ -980,7 +970,8 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 9: return launch_tma<K, 256, 16>(a, s, tiles, dry);
     case 10: return launch_ec<K, 12>(a, s, tiles, dry);
     case 11: return launch_ec<K, 8>(a, s, tiles, dry);
-    default: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
+    case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
+    default: return launch_ec<K, 12>(a, s, tiles, dry);
   }
   }
 }

@@ -127,6 +127,66 @@ __global__ void __launch_bounds__(kRows, 4)
   }
 }
 
+// Warp-independent variant of spmv_seq_kernel: each warp owns 32
+// consecutive rows and its own shared-memory product buffer, so the
+// load → product → sequential-sum phases of different warps interleave freely
+// (only __syncwarp, no CTA barrier).  Same arithmetic, bit-exact.
+constexpr int kWarpChunk = 512;  // products per warp per chunk (4 KB)
+constexpr int kWarpsPerCta = 8;
+
+template <typename P, typename C, typename Q>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 4)
+    spmv_wseq_kernel(const P* __restrict__ row_ptr, const C* __restrict__ col,
+                     const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
+                     int64_t row1, const Q* __restrict__ perm, double* __restrict__ y) {
+  __shared__ double prod_all[kWarpsPerCta][kWarpChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* prod = prod_all[warp];
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+  const int64_t w0 = row0 + ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+  if (w0 >= row1) return;
+  const int64_t w1 = min(w0 + 32, row1);
+  const int64_t r = w0 + lane;
+  const int64_t nz0 = ld_idx(row_ptr, w0);
+  const int64_t nz1 = ld_idx(row_ptr, w1);
+  int64_t rs = 0, re = 0;
+  if (r < row1) {
+    rs = ld_idx(row_ptr, r);
+    re = ld_idx(row_ptr, r + 1);
+  }
+  double acc = 0.0;
+  for (int64_t cs = nz0; cs < nz1; cs += kWarpChunk) {
+    const int n = (int)min((int64_t)kWarpChunk, nz1 - cs);
+#pragma unroll
+    for (int u0 = 0; u0 < kWarpChunk / 32; u0 += 8) {
+      int64_t c[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + (u0 + u) * 32;
+        if (k < n) {
+          c[u] = ld_stream_idx(col + cs + k, stream);
+          v[u] = ld_stream(val + cs + k, stream);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + (u0 + u) * 32;
+        if (k < n) prod[swz(k)] = __dmul_rn(v[u], ld_keep(x + c[u], keep));
+      }
+      if (u0 + 8 >= (n + 31) / 32) break;  // rest of the chunk is empty
+    }
+    __syncwarp();
+    const int64_t a = max(rs, cs), b = min(re, cs + n);
+    for (int64_t k = a; k < b; ++k) acc = __dadd_rn(acc, prod[swz((int)(k - cs))]);
+    __syncwarp();
+  }
+  if (r < row1) {
+    if (perm) y[(int64_t)perm[r]] = acc;
+    else y[r - row0] = acc;
+  }
+}
+
 // warp-per-row tree reduction (not bit-exact)
 template <typename P, typename C, typename Q>
 __global__ void __launch_bounds__(256)
@@ -177,6 +237,14 @@ __global__ void csr_validate_kernel(const P* __restrict__ row_ptr, const C* __re
 
 int idx_size_ok(int code) { return code == HB_I32 || code == HB_I64; }
 
+int spmv_variant() {
+  static int v = [] {
+    const char* e = getenv("HB_SPMV_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <typename P, typename C, typename Q>
 int launch_spmv(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
                 int64_t row1, const void* pm, double* y, int mode, cudaStream_t s) {
@@ -187,7 +255,10 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
   auto p = reinterpret_cast<const P*>(rp);
   auto c = reinterpret_cast<const C*>(ci);
   auto q = reinterpret_cast<const Q*>(pm);
-  if (mode == 1) {
+  if (mode == 2 || (mode == 0 && spmv_variant() == 1)) {
+    const int64_t blocks = ceil_div(rows, 32 * kWarpsPerCta);
+    spmv_wseq_kernel<P, C, Q><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p, c, v, x, row0, row1, q, y);
+  } else if (mode == 1) {
     int64_t blocks = ceil_div(rows, 8);
     if (blocks > (int64_t)di.sms * 8) blocks = (int64_t)di.sms * 8;
     spmv_warp_kernel<P, C, Q><<<(int)blocks, 256, 0, s>>>(p, c, v, x, row0, row1, q, y);
@@ -233,7 +304,7 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
   HB_CHECK_ARG(perm == nullptr || idx_size_ok(perm_code), "perm must be int32 or int64");
   HB_CHECK_ARG(row0 >= 0 && row1 >= row0, "bad row range [%lld, %lld)", (long long)row0, (long long)row1);
   HB_CHECK_ARG(cols >= 0, "cols must be >= 0");
-  HB_CHECK_ARG(mode == 0 || mode == 1, "unknown SpMV mode %d", mode);
+  HB_CHECK_ARG(mode >= 0 && mode <= 2, "unknown SpMV mode %d", mode);
   if (row1 == row0) return HB_OK;
   HB_CHECK_ARG(row_ptr && y && x, "NULL row_ptr, x or y");
   const bool dev = flags & HB_DEVICE_PTRS;

@@ -67,9 +67,18 @@ __device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra
 // and every thread has kChains independent dependent-load chains in flight.
 constexpr int kChains = 4;
 
-template <typename S>
-__device__ __forceinline__ int64_t ld_succ(const S* p) {
-  return (int64_t)__ldg(p);
+// Successor reads are random: load them L2-only (.cg).  The read-only
+// (.nc / __ldg) path promotes every L1 miss to a full 128-byte line, i.e.
+// four 32-byte sectors of DRAM traffic for one useful 4-byte successor.
+__device__ __forceinline__ int64_t ld_succ(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_succ(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
 }
 
 __device__ __forceinline__ void st_stream(uint64_t* p, uint64_t v) {

@@ -714,13 +714,14 @@ __global__ void scan_hist_kernel(const uint32_t* __restrict__ hist, uint32_t* __
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <typename K, bool HAS_V, int I>
-__global__ void __launch_bounds__(512, 2)
+template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE>
+__global__ void __launch_bounds__(T, 1024 / T)
     onesweep_ec_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                        uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
                        const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
                        uint32_t* __restrict__ tile_counter) {
-  constexpr int T = 512, W = T / 32, TILE = T * I;
+  constexpr int W = T / 32, TILE = T * I;
+  static_assert(T > 256, "warps 8.. rank while warps 0-7 look back");
   __shared__ uint32_t s_base[W][256];   // per-warp counts → per-(warp, digit) tile positions
   __shared__ uint32_t s_run[W][256];    // warp-local running counts for the stable ranking
   __shared__ uint32_t s_goff[256];
@@ -766,16 +767,33 @@ __global__ void __launch_bounds__(512, 2)
   const uint32_t lt = lanemask_lt();
   auto rank_keys = [&]() {
     uint32_t* wr = s_run[warp];
+    if constexpr (TWO_PHASE) {
+      // all rows' peer masks first (independent → ILP), then the counter chain
+      uint32_t pm[I];
 #pragma unroll
-    for (int i = 0; i < I; ++i) {
-      const uint32_t d = dig[i];
-      const uint32_t peers = match_digit8(d);
-      const uint32_t below = __popc(peers & lt);
-      const uint32_t pre = wr[d];
-      __syncwarp();
-      if ((peers & ~(lt | (1u << lane))) == 0) wr[d] = pre + below + 1u;
-      __syncwarp();
-      rank[i] = pre + below;
+      for (int i = 0; i < I; ++i) pm[i] = match_digit8(dig[i]);
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        const uint32_t d = dig[i];
+        const uint32_t below = __popc(pm[i] & lt);
+        const uint32_t pre = wr[d];
+        __syncwarp();
+        if ((pm[i] & ~(lt | (1u << lane))) == 0) wr[d] = pre + below + 1u;
+        __syncwarp();
+        rank[i] = pre + below;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        const uint32_t d = dig[i];
+        const uint32_t peers = match_digit8(d);
+        const uint32_t below = __popc(peers & lt);
+        const uint32_t pre = wr[d];
+        __syncwarp();
+        if ((peers & ~(lt | (1u << lane))) == 0) wr[d] = pre + below + 1u;
+        __syncwarp();
+        rank[i] = pre + below;
+      }
     }
   };
 
@@ -852,19 +870,19 @@ struct PassArgs {
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
 };
 
-template <typename K, int I>
+template <typename K, int I, int T = 512, bool TWO = false>
 int launch_ec(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
-  const int64_t tiles = ceil_div(a.n, (int64_t)512 * I);
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
   *tiles_out = tiles;
   if (dry) return HB_OK;
-  const size_t smem = (size_t)512 * I * sizeof(K) + (a.vin ? (size_t)512 * I * 4 : 0);
+  const size_t smem = (size_t)T * I * sizeof(K) + (a.vin ? (size_t)T * I * 4 : 0);
   if (a.vin) {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, true, I><<<(unsigned)tiles, 512, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, true, I, T, TWO><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   } else {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, false, I><<<(unsigned)tiles, 512, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, false, I, T, TWO><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   }
   return check_launch();
@@ -970,6 +988,10 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 9: return launch_tma<K, 256, 16>(a, s, tiles, dry);
     case 10: return launch_ec<K, 12>(a, s, tiles, dry);
     case 11: return launch_ec<K, 8>(a, s, tiles, dry);
+    case 13: return launch_ec<K, 16, 384>(a, s, tiles, dry);
+    case 14: return launch_ec<K, 12, 512, true>(a, s, tiles, dry);
+    case 15: return launch_ec<K, 16, 384, true>(a, s, tiles, dry);
+    case 16: return launch_ec<K, 20, 384>(a, s, tiles, dry);
     case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
     default: return launch_ec<K, 12>(a, s, tiles, dry);
   }

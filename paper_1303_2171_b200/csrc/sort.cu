@@ -992,6 +992,10 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 14: return launch_ec<K, 12, 512, true>(a, s, tiles, dry);
     case 15: return launch_ec<K, 16, 384, true>(a, s, tiles, dry);
     case 16: return launch_ec<K, 20, 384>(a, s, tiles, dry);
+    case 17: return launch_ec<K, 24, 384>(a, s, tiles, dry);
+    case 18: return launch_ec<K, 16, 512>(a, s, tiles, dry);
+    case 19: return launch_ec<K, 16, 640>(a, s, tiles, dry);
+    case 20: return launch_ec<K, 28, 384>(a, s, tiles, dry);
     case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
     default: return launch_ec<K, 12>(a, s, tiles, dry);
   }

@@ -997,7 +997,7 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 19: return launch_ec<K, 16, 640>(a, s, tiles, dry);
     case 20: return launch_ec<K, 28, 384>(a, s, tiles, dry);
     case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
-    default: return launch_ec<K, 12>(a, s, tiles, dry);
+    default: return launch_ec<K, 20, 384>(a, s, tiles, dry);  // best measured (round 1)
   }
   }
 }

@@ -113,6 +113,15 @@ int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_idx, int col_
 /* CsrMatrix invariants (kernels_irregular.py:44-60) checked on the device:
  * *flags_out |= 1 bad row_ptr ends, 2 decreasing row_ptr, 4 column out of
  * range, 8 columns not strictly increasing within a row.                   */
+/* Device spmv_preprocess (kernels_irregular.py:171-203): perm_out = the
+ * stable argsort of the row lengths (hb_sort with a row-index payload),
+ * new_row_ptr = exclusive scan of the sorted lengths, rows gathered into
+ * new_col/new_values.  Index types follow ptr_code / col_code / perm_code.
+ * Device pointers only.                                                    */
+int hb_spmv_preprocess(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
+                       const double* values, int64_t rows, void* perm_out, int perm_code,
+                       void* new_row_ptr, void* new_col, double* new_values, int flags, void* stream);
+
 int hb_csr_validate(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
                     int64_t rows, int64_t nnz, int64_t cols, uint32_t* flags_out, int flags,
                     void* stream);

@@ -46,6 +46,7 @@ _SIGNATURES: dict[str, list] = {
     "hb_hist": [_vp, _int, _i64, _i32, _vp, _int, _vp],
     "hb_spmv_csr": [_vp, _int, _vp, _int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _vp, _int, _int, _vp],
     "hb_csr_validate": [_vp, _int, _vp, _int, _i64, _i64, _i64, _vp, _int, _vp],
+    "hb_spmv_preprocess": [_vp, _int, _vp, _int, _vp, _i64, _vp, _int, _vp, _vp, _vp, _int, _vp],
     "hb_bilateral_u8": [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _int, _int, _vp],
     "hb_sort": [_vp, _vp, _int, _vp, _vp, _i64, _vp, _int, _vp],
     "hb_sort_bounds": [_vp, _int, _vp, _i64, _vp, _vp, _i32, _vp, _int, _vp],

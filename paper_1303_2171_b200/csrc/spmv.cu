@@ -394,3 +394,164 @@ extern "C" int hb_csr_validate(const void* row_ptr, int ptr_code, const void* co
   *flags_out = host;
   return HB_OK;
 }
+
+// ------------------------------------------------------------------ preprocess
+// Device spmv_preprocess (kernels_irregular.py:171-203): rows stably sorted
+// by nnz (hb_sort of the row lengths with a row-index payload), new row_ptr
+// by an exclusive scan, rows gathered warp-per-row.
+namespace hb {
+namespace {
+
+template <typename P>
+__global__ void row_len_kernel(const P* __restrict__ rp, int64_t rows, uint32_t* __restrict__ len,
+                               uint32_t* __restrict__ idx) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    len[r] = (uint32_t)((int64_t)rp[r + 1] - (int64_t)rp[r]);
+    idx[r] = (uint32_t)r;
+  }
+}
+
+// exclusive scan of u32 lengths into row_ptr (int64 or int32), 3 phases
+constexpr int kScanT = 512, kScanI = 8, kScanTile = kScanT * kScanI;
+
+__global__ void __launch_bounds__(kScanT) scan_tile_sums(const uint32_t* __restrict__ v, int64_t n,
+                                                         int64_t* __restrict__ sums) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int64_t t = 0;
+  for (int i = 0; i < kScanI; ++i) {
+    const int64_t k = base + i * kScanT + threadIdx.x;
+    if (k < n) t += v[k];
+  }
+  __shared__ int64_t ws[kScanT / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t a = 0;
+    for (int w = 0; w < kScanT / 32; ++w) a += ws[w];
+    sums[blockIdx.x] = a;
+  }
+}
+
+__global__ void scan_sums_serial(int64_t* __restrict__ sums, int64_t nb) {
+  // nb = rows / 4096: a few thousand values, one thread is fine
+  int64_t run = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t c = sums[b];
+    sums[b] = run;
+    run += c;
+  }
+  sums[nb] = run;
+}
+
+template <typename P>
+__global__ void __launch_bounds__(kScanT) scan_tile_apply(const uint32_t* __restrict__ v, int64_t n,
+                                                          const int64_t* __restrict__ sums,
+                                                          P* __restrict__ out) {
+  // blocked layout: thread t owns elements [t*kScanI, (t+1)*kScanI) of the tile
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanI;
+  uint32_t x[kScanI];
+  int64_t tsum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanI; ++i) {
+    x[i] = base + i < n ? v[base + i] : 0u;
+    tsum += x[i];
+  }
+  // block exclusive scan of tsum
+  __shared__ int64_t ws[kScanT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  int64_t wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += ws[w];
+  int64_t run = sums[blockIdx.x] + wpre + incl - tsum;
+#pragma unroll
+  for (int i = 0; i < kScanI; ++i) {
+    if (base + i < n) out[base + i] = (P)run;
+    run += x[i];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanT - 1) out[n] = (P)sums[gridDim.x];
+}
+
+template <typename PI, typename CI, typename PO, typename CO, typename QO>
+__global__ void gather_rows_kernel(const PI* __restrict__ rp, const CI* __restrict__ col,
+                                   const double* __restrict__ val, int64_t rows,
+                                   const uint32_t* __restrict__ perm, const PO* __restrict__ nrp,
+                                   CO* __restrict__ ncol, double* __restrict__ nval,
+                                   QO* __restrict__ perm_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const int64_t old = perm[r];
+    const int64_t a = (int64_t)rp[old], b = (int64_t)rp[old + 1];
+    const int64_t d = (int64_t)nrp[r];
+    for (int64_t k = a + lane; k < b; k += 32) {
+      ncol[d + (k - a)] = (CO)col[k];
+      nval[d + (k - a)] = val[k];
+    }
+    if (lane == 0) perm_out[r] = (QO)old;
+  }
+}
+
+template <typename PI, typename CI, typename PO, typename CO, typename QO>
+int preprocess_impl(const void* rp, const void* col, const double* val, int64_t rows, void* perm_out,
+                    void* nrp, void* ncol, double* nval, cudaStream_t s) {
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  DevBuf len, idx;
+  HB_TRY(alloc(&len, (size_t)rows * 4, s));
+  HB_TRY(alloc(&idx, (size_t)rows * 4, s));
+  int64_t g = ceil_div(rows, 256);
+  if (g > (int64_t)di.sms * 16) g = (int64_t)di.sms * 16;
+  row_len_kernel<PI><<<(int)g, 256, 0, s>>>((const PI*)rp, rows, len.as<uint32_t>(), idx.as<uint32_t>());
+  HB_TRY(check_launch());
+  int32_t passes = 0;
+  HB_TRY(hb_sort(len.ptr, len.ptr, HB_U32, idx.as<uint32_t>(), idx.as<uint32_t>(), rows, &passes,
+                 HB_DEVICE_PTRS | HB_ASYNC, s));
+  const int64_t nb = ceil_div(rows, kScanTile);
+  DevBuf sums;
+  HB_TRY(alloc(&sums, (size_t)(nb + 1) * 8, s));
+  scan_tile_sums<<<(unsigned)nb, kScanT, 0, s>>>(len.as<uint32_t>(), rows, sums.as<int64_t>());
+  scan_sums_serial<<<1, 1, 0, s>>>(sums.as<int64_t>(), nb);
+  scan_tile_apply<PO><<<(unsigned)nb, kScanT, 0, s>>>(len.as<uint32_t>(), rows, sums.as<int64_t>(), (PO*)nrp);
+  HB_TRY(check_launch());
+  int64_t gw = ceil_div(rows, 8);
+  if (gw > (int64_t)di.sms * 32) gw = (int64_t)di.sms * 32;
+  gather_rows_kernel<PI, CI, PO, CO, QO><<<(int)gw, 256, 0, s>>>(
+      (const PI*)rp, (const CI*)col, val, rows, idx.as<uint32_t>(), (const PO*)nrp, (CO*)ncol, nval, (QO*)perm_out);
+  return check_launch();
+}
+
+}  // namespace
+}  // namespace hb
+
+extern "C" int hb_spmv_preprocess(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
+                                  const double* values, int64_t rows, void* perm_out, int perm_code,
+                                  void* new_row_ptr, void* new_col, double* new_values, int flags,
+                                  void* stream) {
+  using namespace hb;
+  HB_CHECK_ARG(idx_size_ok(ptr_code) && idx_size_ok(col_code) && idx_size_ok(perm_code),
+               "index arrays must be int32 or int64");
+  HB_CHECK_ARG(rows >= 1 && rows < (1ll << 30), "rows out of range");
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_spmv_preprocess works on device arrays");
+  cudaStream_t s = as_stream(stream);
+  int rc;
+  // output index types follow the inputs (perm: perm_code)
+#define HB_PP(PI, CI, QO) preprocess_impl<PI, CI, PI, CI, QO>(row_ptr, col_idx, values, rows, perm_out, new_row_ptr, new_col, new_values, s)
+  const bool p4 = ptr_code == HB_I32, c4 = col_code == HB_I32, q4 = perm_code == HB_I32;
+  if (p4 && c4) rc = q4 ? HB_PP(int32_t, int32_t, int32_t) : HB_PP(int32_t, int32_t, int64_t);
+  else if (p4) rc = q4 ? HB_PP(int32_t, int64_t, int32_t) : HB_PP(int32_t, int64_t, int64_t);
+  else if (c4) rc = q4 ? HB_PP(int64_t, int32_t, int32_t) : HB_PP(int64_t, int32_t, int64_t);
+  else rc = q4 ? HB_PP(int64_t, int64_t, int32_t) : HB_PP(int64_t, int64_t, int64_t);
+#undef HB_PP
+  if (rc != HB_OK) return rc;
+  return finish(flags, s);
+}

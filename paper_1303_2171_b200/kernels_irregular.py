@@ -168,7 +168,7 @@ class SpmvPrep:
     split_row: int
 
     def __post_init__(self) -> None:
-        perm = to_host(self.perm)
+        perm = np.asarray(to_host(self.perm), dtype=np.int64)
         n = self.permuted.rows
         if perm.shape != (n,) or not np.array_equal(np.sort(perm), np.arange(n)):
             raise StructuralError("perm must be a permutation of the row indices")
@@ -193,11 +193,15 @@ def spmv_preprocess(m: CsrMatrix, platform: Platform, share: WorkShare | None = 
     the two modeled throughputs, or `searchsorted(cum, f·total, 'left')` for
     an explicit share (:186-203).  Device matrices are permuted on the host
     index arrays and re-uploaded (one-time prep)."""
-    row_nnz = m.row_nnz
-    perm = np.argsort(row_nnz, kind="stable")
-    permuted = _permute_rows_host(m.to_host(), perm)
-    cum = np.zeros(m.rows + 1, dtype=np.float64)
-    np.cumsum(row_nnz[perm], out=cum[1:])
+    if m.on_device:
+        perm, permuted = _device_preprocess(m)
+        cum = to_host(permuted.row_ptr).astype(np.float64)
+    else:
+        row_nnz = m.row_nnz
+        perm = np.argsort(row_nnz, kind="stable")
+        permuted = _permute_rows_host(m, perm)
+        cum = np.zeros(m.rows + 1, dtype=np.float64)
+        np.cumsum(row_nnz[perm], out=cum[1:])
     total = cum[-1]
     if share is not None:
         split = int(np.searchsorted(cum, share.fraction_a * total, side="left"))
@@ -205,9 +209,26 @@ def spmv_preprocess(m: CsrMatrix, platform: Platform, share: WorkShare | None = 
         t_a = cum / platform.device_a.throughput
         t_b = (total - cum) / platform.device_b.throughput
         split = int(np.argmin(np.maximum(t_a, t_b)))
-    if m.on_device:
-        permuted = permuted.to_device(np.int32 if m.col_idx.dtype.itemsize == 4 else np.int64)
     return SpmvPrep(permuted, perm, split)
+
+
+def _device_preprocess(m: CsrMatrix):
+    """Row sort + gather on the GPU (hb_spmv_preprocess): returns the
+    permutation (int32 CUDA tensor) and the permuted device matrix."""
+    import torch
+
+    require_gpu()
+    dev = m.row_ptr.device
+    perm = torch.empty(m.rows, dtype=torch.int32, device=dev)
+    nrp = torch.empty(m.rows + 1, dtype=m.row_ptr.dtype, device=dev)
+    ncol = torch.empty_like(m.col_idx)
+    nval = torch.empty_like(m.values)
+    _lib.call(
+        "hb_spmv_preprocess", vp(m.row_ptr.data_ptr()), _index_code(m.row_ptr), vp(m.col_idx.data_ptr()),
+        _index_code(m.col_idx), vp(m.values.data_ptr()), m.rows, vp(perm.data_ptr()), _lib.DTYPE_CODES["i4"],
+        vp(nrp.data_ptr()), vp(ncol.data_ptr()), vp(nval.data_ptr()), _lib.HB_DEVICE_PTRS, current_stream_handle(nrp),
+    )
+    return perm, CsrMatrix(m.rows, m.cols, nrp, ncol, nval)
 
 
 def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int) -> np.ndarray:

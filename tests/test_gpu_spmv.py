@@ -133,3 +133,27 @@ def test_workshared_runner_path():
     perm, permuted, split = ospmv.preprocess(ptr, col, val, 1.0, 3.0, None)
     assert np.array_equal(bits(y), bits(ospmv.hybrid(perm, permuted, split, x)))
     assert report.pure_b_time > 0
+
+
+def test_device_preprocess_matches_host(platform13):
+    import torch
+
+    g = golden("spmv")
+    for i in range(4):
+        m = CsrMatrix(len(g[f"ptr_{i}"]) - 1, len(g[f"x_{i}"]), g[f"ptr_{i}"], g[f"col_{i}"], g[f"val_{i}"])
+        for share in (None, WorkShare.manual(0.0), WorkShare.manual(0.37)):
+            hp = spmv_preprocess(m, platform13, share)
+            dp = spmv_preprocess(m.to_device(np.int64), platform13, share)
+            assert np.array_equal(np.asarray(dp.perm.cpu()), hp.perm) and dp.split_row == hp.split_row
+            assert np.array_equal(dp.permuted.row_ptr.cpu().numpy(), hp.permuted.row_ptr)
+            assert np.array_equal(dp.permuted.col_idx.cpu().numpy(), hp.permuted.col_idx)
+            assert np.array_equal(dp.permuted.values.cpu().numpy(), hp.permuted.values)
+    # larger, int32 indices, then a full device SpMV with the fused un-permute
+    ptr, col, val = ods.csr(200_000, 200_000, 7, 8e-5)
+    m = CsrMatrix(200_000, 200_000, ptr, col, val)
+    x = 2.0 * orng.uniform_floats(orng.mix_seed(7, 0xDEC0), 200_000) - 1.0
+    dp = spmv_preprocess(m.to_device(np.int32), platform13, WorkShare.manual(0.0))
+    y = gpu_spmv(dp.permuted, torch.from_numpy(x).cuda(), 0, m.rows, perm=dp.perm)
+    perm, permuted, split = ospmv.preprocess(ptr, col, val, 1.0, 3.0, 0.0)
+    want = ospmv.hybrid(perm, permuted, split, x)
+    assert np.array_equal(bits(y.cpu().numpy()), bits(want))

@@ -46,8 +46,8 @@ def test_golden_bit_exact_all_shares(platform13):
         import torch
 
         xd = torch.from_numpy(x).cuda()
-        permd = torch.from_numpy(np.asarray(dprep.perm)).cuda()
-        y = gpu_spmv(dprep.permuted, xd, 0, m.rows, perm=permd)
+        assert np.array_equal(dprep.perm.cpu().numpy(), g[f"perm_{i}"])  # device spmv_preprocess
+        y = gpu_spmv(dprep.permuted, xd, 0, m.rows, perm=dprep.perm)
         assert np.array_equal(bits(y.cpu().numpy()), bits(g[f"y_{i}"]))
 
 

@@ -99,6 +99,42 @@ __host__ __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64
   return z ^ (z >> 31);
 }
 
+// mbarrier + bulk-copy (TMA 1-D) helpers: one elected thread arms a barrier
+// with the expected byte count and issues cp.async.bulk; consumers wait on
+// the barrier's phase parity.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(a), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* smem, const void* g, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(g), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s_hint(void* smem, const void* g, uint32_t bytes, uint64_t* bar,
+                                                  uint64_t policy) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(d), "l"(g), "r"(bytes), "r"(b), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace hb

@@ -494,28 +494,6 @@ __global__ void __launch_bounds__(T, 3)
 // (completion on an mbarrier, expect_tx bytes) while all warps work on the
 // current tile.  Tile ids are taken when a tile starts (never two ahead), so
 // a tile's predecessors are always current tiles of other CTAs.
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n}" ::"r"(a), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* smem, const void* g, uint32_t bytes, uint64_t* bar) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(d), "l"(g), "r"(bytes), "r"(b) : "memory");
-}
-
 template <typename K, bool HAS_V, int T, int I>
 __device__ __forceinline__ void tma_stage(K* sk, uint32_t* sv, const K* kin, const uint32_t* vin,
                                           int64_t base, int valid, uint64_t* bar) {

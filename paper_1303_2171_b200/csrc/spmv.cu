@@ -187,6 +187,139 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 4)
   }
 }
 
+// Persistent, bulk-copy pipelined variant (same arithmetic, bit-exact).
+// The matrix stream never passes through the LSU: one elected thread copies
+// each chunk's contiguous val/col ranges into a shared-memory stage with
+// cp.async.bulk (completion on an mbarrier), kStages chunks ahead of the
+// consumers, so HBM streams continuously while all 256 threads spend their
+// LSU slots on the x gathers (L2) and the row sums (smem).
+//   work item = (tile of 256 rows, chunk of <= C products of that tile);
+//   tiles are dealt round-robin (rows are nnz-sorted, so neighbouring tiles
+//   have equal cost); every tile has >= 1 item, so empty rows still write 0.
+// Bulk copies need 16-byte aligned addresses and sizes: a chunk copies the
+// 16-byte blocks covering [cs, cs+n); the element offset of cs inside its
+// block (voff/coff) is recomputed by the consumers.  The copy never reaches
+// past the 16-byte block holding the chunk's last element, so it never leaves
+// the page of a valid byte.
+template <int C, int S>
+struct BulkLayout {
+  static constexpr size_t kVal = (size_t)C * 8 + 16;   // f64 stage (+ alignment slack)
+  static constexpr size_t kCol = (size_t)C * 4 + 16;   // i32 stage
+  static constexpr size_t kStage = kVal + kCol;
+  static constexpr size_t kProd = (size_t)C * 8;        // swizzled products
+  static constexpr size_t kBytes = S * kStage + kProd;
+};
+
+template <typename Q, int C, int S, int MINB>
+__global__ void __launch_bounds__(kRows, MINB)
+    spmv_bulk_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                     const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
+                     int64_t row1, const Q* __restrict__ perm, double* __restrict__ y, int64_t ntiles) {
+  using L = BulkLayout<C, S>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[S];
+  double* prod = reinterpret_cast<double*>(smem + S * L::kStage);
+  auto sval = [&](int s) { return reinterpret_cast<double*>(smem + s * L::kStage); };
+  auto scol = [&](int s) { return reinterpret_cast<int32_t*>(smem + s * L::kStage + L::kVal); };
+  const int tid = threadIdx.x;
+  const uint64_t keep = l2_evict_last();
+
+  // producer cursor (thread 0 only): tile, chunk start, tile nnz end
+  int64_t p_tile = blockIdx.x, p_cs = 0, p_nz1 = 0;
+  auto p_issue = [&](int s) {
+    // arm stage s with the current item and advance the cursor
+    const int n = (int)min((int64_t)C, p_nz1 - p_cs);
+    const uintptr_t v0 = (uintptr_t)(val + p_cs) & ~(uintptr_t)15, v1 = ((uintptr_t)(val + p_cs + n) + 15) & ~(uintptr_t)15;
+    const uintptr_t c0 = (uintptr_t)(col + p_cs) & ~(uintptr_t)15, c1 = ((uintptr_t)(col + p_cs + n) + 15) & ~(uintptr_t)15;
+    const uint32_t vb = n ? (uint32_t)(v1 - v0) : 0u, cb = n ? (uint32_t)(c1 - c0) : 0u;
+    mbar_expect_tx(&full[s], vb + cb);
+    if (n) {
+      tma_bulk_g2s(sval(s), (const void*)v0, vb, &full[s]);
+      tma_bulk_g2s(scol(s), (const void*)c0, cb, &full[s]);
+    }
+    p_cs += C;
+    if (p_cs >= p_nz1) {  // next tile
+      p_tile += gridDim.x;
+      if (p_tile < ntiles) {
+        const int64_t b0 = row0 + p_tile * kRows;
+        p_cs = row_ptr[b0];
+        p_nz1 = row_ptr[min(b0 + kRows, row1)];
+      }
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (p_tile < ntiles) {
+      const int64_t b0 = row0 + p_tile * kRows;
+      p_cs = row_ptr[b0];
+      p_nz1 = row_ptr[min(b0 + kRows, row1)];
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (p_tile < ntiles) p_issue(s);
+    }
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b0 = row0 + tile * kRows;
+    const int64_t b1 = min(b0 + kRows, row1);
+    const int64_t r = b0 + tid;
+    const int64_t nz0 = row_ptr[b0], nz1 = row_ptr[b1];
+    int64_t rs = 0, re = 0;
+    if (r < b1) {
+      rs = row_ptr[r];
+      re = row_ptr[r + 1];
+    }
+    double acc = 0.0;
+    int64_t cs = nz0;
+    do {
+      const int n = (int)min((int64_t)C, nz1 - cs);
+      mbar_wait(&full[stage], phase);
+      const double* sv = sval(stage) + (((uintptr_t)(val + cs) & 15) >> 3);
+      const int32_t* sc = scol(stage) + (((uintptr_t)(col + cs) & 15) >> 2);
+      constexpr int U = C / kRows;
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = tid + u * kRows;
+        c[u] = k < n ? sc[k] : 0;
+      }
+      double g[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = tid + u * kRows;
+        if (k < n) g[u] = ld_keep(x + c[u], keep);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = tid + u * kRows;
+        if (k < n) prod[swz(k)] = __dmul_rn(sv[k], g[u]);
+      }
+      __syncthreads();
+      const int64_t a = max(rs, cs), b = min(re, cs + n);
+      for (int64_t k = a; k < b; ++k) acc = __dadd_rn(acc, prod[swz((int)(k - cs))]);
+      __syncthreads();  // stage and prod free
+      if (tid == 0 && p_tile < ntiles) {
+        fence_proxy_async_smem();
+        p_issue(stage);
+      }
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      cs += C;
+    } while (cs < nz1);
+    if (r < b1) {
+      if (perm) y[(int64_t)perm[r]] = acc;
+      else y[r - row0] = acc;
+    }
+  }
+}
+
 // warp-per-row tree reduction (not bit-exact)
 template <typename P, typename C, typename Q>
 __global__ void __launch_bounds__(256)
@@ -245,6 +378,20 @@ int spmv_variant() {
   return v;
 }
 
+template <typename Q, int C, int S, int MINB>
+int launch_bulk(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
+                int64_t row1, const void* pm, double* y, const DeviceInfo& di, cudaStream_t s) {
+  using L = BulkLayout<C, S>;
+  auto k = spmv_bulk_kernel<Q, C, S, MINB>;
+  HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes));
+  const int64_t ntiles = ceil_div(row1 - row0, kRows);
+  int64_t grid = (int64_t)di.sms * MINB;
+  if (grid > ntiles) grid = ntiles;
+  k<<<(unsigned)grid, kRows, L::kBytes, s>>>(reinterpret_cast<const int32_t*>(rp), reinterpret_cast<const int32_t*>(ci),
+                                             v, x, row0, row1, reinterpret_cast<const Q*>(pm), y, ntiles);
+  return check_launch();
+}
+
 template <typename P, typename C, typename Q>
 int launch_spmv(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
                 int64_t row1, const void* pm, double* y, int mode, cudaStream_t s) {
@@ -255,7 +402,17 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
   auto p = reinterpret_cast<const P*>(rp);
   auto c = reinterpret_cast<const C*>(ci);
   auto q = reinterpret_cast<const Q*>(pm);
-  if (mode == 2 || (mode == 0 && spmv_variant() == 1)) {
+  const int var = spmv_variant();
+  if (mode == 0 && sizeof(P) == 4 && sizeof(C) == 4 && var >= 2 && var <= 6) {
+    switch (var) {
+      case 2: return launch_bulk<Q, 2048, 3, 2>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 3: return launch_bulk<Q, 2048, 2, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 4: return launch_bulk<Q, 1024, 4, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 5: return launch_bulk<Q, 4096, 2, 1>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      default: return launch_bulk<Q, 1024, 2, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
+    }
+  }
+  if (mode == 2 || (mode == 0 && var == 1)) {
     const int64_t blocks = ceil_div(rows, 32 * kWarpsPerCta);
     spmv_wseq_kernel<P, C, Q><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p, c, v, x, row0, row1, q, y);
   } else if (mode == 1) {

@@ -257,7 +257,7 @@ class SpmvBench:
 
     name = "spmv"
     unit = "GFLOP/s"
-    kernel = "spmv_seq_kernel"
+    kernel = "spmv_lpr_kernel"
 
     def __init__(self, rows: int = 1_000_000, density: float = 1.6e-5, seed: int = 42):
         self.rows, self.density, self.seed = rows, density, seed

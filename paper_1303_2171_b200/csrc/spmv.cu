@@ -6,7 +6,9 @@
 // HB_SPMV_SEQ (default) reproduces the reference arithmetic bit for bit:
 // every product is one rounded fp64 multiply and every row is summed left to
 // right from +0.0 with rounded adds, no FMA contraction (the reference's
-// `np.bincount(row_of, weights=values*x[col])`).
+// `np.bincount(row_of, weights=values*x[col])`).  Two kernels implement it:
+// spmv_lpr_kernel (int32 row_ptr/col_idx, the layout spmv_preprocess emits;
+// see its comment) and the generic spmv_seq_kernel (any index width):
 //   * one CTA = ROWS consecutive rows; its nnz range is streamed in chunks of
 //     CHUNK products: coalesced loads of values/col_idx (each warp load moves
 //     256/128 contiguous bytes), x gathered through the read-only path (x is
@@ -127,183 +129,141 @@ __global__ void __launch_bounds__(kRows, 4)
   }
 }
 
-// Warp-independent variant of spmv_seq_kernel: each warp owns 32
-// consecutive rows and its own shared-memory product buffer, so the
-// load → product → sequential-sum phases of different warps interleave freely
-// (only __syncwarp, no CTA barrier).  Same arithmetic, bit-exact.
-constexpr int kWarpChunk = 512;  // products per warp per chunk (4 KB)
-constexpr int kWarpsPerCta = 8;
-
-template <typename P, typename C, typename Q>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 4)
-    spmv_wseq_kernel(const P* __restrict__ row_ptr, const C* __restrict__ col,
-                     const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
-                     int64_t row1, const Q* __restrict__ perm, double* __restrict__ y) {
-  __shared__ double prod_all[kWarpsPerCta][kWarpChunk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* prod = prod_all[warp];
-  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
-  const int64_t w0 = row0 + ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
-  if (w0 >= row1) return;
-  const int64_t w1 = min(w0 + 32, row1);
-  const int64_t r = w0 + lane;
-  const int64_t nz0 = ld_idx(row_ptr, w0);
-  const int64_t nz1 = ld_idx(row_ptr, w1);
-  int64_t rs = 0, re = 0;
-  if (r < row1) {
-    rs = ld_idx(row_ptr, r);
-    re = ld_idx(row_ptr, r + 1);
-  }
-  double acc = 0.0;
-  for (int64_t cs = nz0; cs < nz1; cs += kWarpChunk) {
-    const int n = (int)min((int64_t)kWarpChunk, nz1 - cs);
-#pragma unroll
-    for (int u0 = 0; u0 < kWarpChunk / 32; u0 += 8) {
-      int64_t c[8];
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = lane + (u0 + u) * 32;
-        if (k < n) {
-          c[u] = ld_stream_idx(col + cs + k, stream);
-          v[u] = ld_stream(val + cs + k, stream);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = lane + (u0 + u) * 32;
-        if (k < n) prod[swz(k)] = __dmul_rn(v[u], ld_keep(x + c[u], keep));
-      }
-      if (u0 + 8 >= (n + 31) / 32) break;  // rest of the chunk is empty
-    }
-    __syncwarp();
-    const int64_t a = max(rs, cs), b = min(re, cs + n);
-    for (int64_t k = a; k < b; ++k) acc = __dadd_rn(acc, prod[swz((int)(k - cs))]);
-    __syncwarp();
-  }
-  if (r < row1) {
-    if (perm) y[(int64_t)perm[r]] = acc;
-    else y[r - row0] = acc;
-  }
-}
-
-// Persistent, bulk-copy pipelined variant (same arithmetic, bit-exact).
-// The matrix stream never passes through the LSU: one elected thread copies
-// each chunk's contiguous val/col ranges into a shared-memory stage with
-// cp.async.bulk (completion on an mbarrier), kStages chunks ahead of the
-// consumers, so HBM streams continuously while all 256 threads spend their
-// LSU slots on the x gathers (L2) and the row sums (smem).
-//   work item = (tile of 256 rows, chunk of <= C products of that tile);
-//   tiles are dealt round-robin (rows are nnz-sorted, so neighbouring tiles
-//   have equal cost); every tile has >= 1 item, so empty rows still write 0.
-// Bulk copies need 16-byte aligned addresses and sizes: a chunk copies the
-// 16-byte blocks covering [cs, cs+n); the element offset of cs inside its
-// block (voff/coff) is recomputed by the consumers.  The copy never reaches
-// past the 16-byte block holding the chunk's last element, so it never leaves
-// the page of a valid byte.
-template <int C, int S>
-struct BulkLayout {
-  static constexpr size_t kVal = (size_t)C * 8 + 16;   // f64 stage (+ alignment slack)
-  static constexpr size_t kCol = (size_t)C * 4 + 16;   // i32 stage
+// Lane-per-row, bulk-copy fed kernel (bit-exact; the default for int32
+// indices).  What bounds it (measured, scripts/micro/*.cu):
+//   * every nnz costs one random 8-byte x gather = one L2 sector request; an
+//     SM issues <= ~0.9 such requests per clock (16M gathers alone: 62 us on
+//     148 SMs), and together with the 200 MB matrix stream the floor is
+//     ~72 us (micro: gathers + a coalesced 12 B/nnz stream);
+//   * in-flight gather misses occupy L1: with less than ~100 KB of L1 left
+//     over by the shared-memory carveout the gather rate halves, so shared
+//     memory is kept to the bulk-copy stages and the carveout is set to
+//     exactly what the resident CTAs need.
+// Structure:
+//   * a warp tile = 32 consecutive (nnz-sorted) rows, lane i owns row i;
+//     tiles are dealt round-robin over all warps of the persistent grid;
+//   * work item = chunk of <= CW nnz of a tile; lane 0 streams the val/col
+//     ranges of the warp's next S items into the warp's private smem stages
+//     with cp.async.bulk (per-warp mbarriers, expect_tx bytes) — the matrix
+//     stream never occupies LSU request slots, which the gathers need;
+//   * each lane walks its own row's slice of an item in order, B gathers in
+//     flight per batch: acc = acc + val*x[col], rounded fp64 ops, no FMA —
+//     the reference's bincount arithmetic — with no product buffer or
+//     transposition through shared memory;
+//   * tile bounds (producer) and row bounds + perm (consumers) are loaded
+//     one tile ahead; the perm scatter y[perm[r]] is fused into the store.
+// Bulk copies need 16-byte aligned addresses and sizes: an item copies the
+// 16-byte blocks covering [cs, cs+n) and the consumers re-derive the offset of
+// cs inside its block.  The copy never reaches past the 16-byte block holding
+// the item's last element, so it never leaves the page of a valid byte.
+template <int CW, int S, int WARPS>
+struct LprLayout {
+  static constexpr size_t kVal = (size_t)CW * 8 + 16;  // f64 stage (+ alignment slack)
+  static constexpr size_t kCol = (size_t)CW * 4 + 16;  // i32 stage
   static constexpr size_t kStage = kVal + kCol;
-  static constexpr size_t kProd = (size_t)C * 8;        // swizzled products
-  static constexpr size_t kBytes = S * kStage + kProd;
+  static constexpr size_t kWarp = S * kStage;
+  static constexpr size_t kBytes = WARPS * kWarp;
 };
 
-template <typename Q, int C, int S, int MINB>
-__global__ void __launch_bounds__(kRows, MINB)
-    spmv_bulk_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                     const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
-                     int64_t row1, const Q* __restrict__ perm, double* __restrict__ y, int64_t ntiles) {
-  using L = BulkLayout<C, S>;
+template <typename Q, int CW, int S, int WARPS, int MINB, int B>
+__global__ void __launch_bounds__(32 * WARPS, MINB)
+    spmv_lpr_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                    const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
+                    int64_t row1, const Q* __restrict__ perm, double* __restrict__ y, int64_t ntiles) {
+  using L = LprLayout<CW, S, WARPS>;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[S];
-  double* prod = reinterpret_cast<double*>(smem + S * L::kStage);
-  auto sval = [&](int s) { return reinterpret_cast<double*>(smem + s * L::kStage); };
-  auto scol = [&](int s) { return reinterpret_cast<int32_t*>(smem + s * L::kStage + L::kVal); };
-  const int tid = threadIdx.x;
+  __shared__ __align__(8) uint64_t full_all[WARPS][S];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wsm = smem + warp * L::kWarp;
+  uint64_t* full = full_all[warp];
+  auto sval = [&](int s) { return reinterpret_cast<double*>(wsm + s * L::kStage); };
+  auto scol = [&](int s) { return reinterpret_cast<int32_t*>(wsm + s * L::kStage + L::kVal); };
   const uint64_t keep = l2_evict_last();
+  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+  const int64_t first = (int64_t)blockIdx.x * WARPS + warp;
+  if (first >= ntiles) return;
+  auto tile_nz = [&](int64_t t, int64_t* a, int64_t* b) {
+    const int64_t r0 = row0 + t * 32;
+    *a = row_ptr[r0];
+    *b = row_ptr[min(r0 + 32, row1)];
+  };
 
-  // producer cursor (thread 0 only): tile, chunk start, tile nnz end
-  int64_t p_tile = blockIdx.x, p_cs = 0, p_nz1 = 0;
+  // ---- producer (lane 0): item cursor + prefetched bounds of the tile after
+  int64_t p_tile = first, p_cs = 0, p_nz1 = 0, q_nz0 = 0, q_nz1 = 0;
   auto p_issue = [&](int s) {
-    // arm stage s with the current item and advance the cursor
-    const int n = (int)min((int64_t)C, p_nz1 - p_cs);
+    const int n = (int)min((int64_t)CW, p_nz1 - p_cs);
     const uintptr_t v0 = (uintptr_t)(val + p_cs) & ~(uintptr_t)15, v1 = ((uintptr_t)(val + p_cs + n) + 15) & ~(uintptr_t)15;
     const uintptr_t c0 = (uintptr_t)(col + p_cs) & ~(uintptr_t)15, c1 = ((uintptr_t)(col + p_cs + n) + 15) & ~(uintptr_t)15;
     const uint32_t vb = n ? (uint32_t)(v1 - v0) : 0u, cb = n ? (uint32_t)(c1 - c0) : 0u;
-    mbar_expect_tx(&full[s], vb + cb);
+    mbar_expect_tx(&full[s], vb + cb);  // 0 bytes (empty tile) completes the phase at once
     if (n) {
       tma_bulk_g2s(sval(s), (const void*)v0, vb, &full[s]);
       tma_bulk_g2s(scol(s), (const void*)c0, cb, &full[s]);
     }
-    p_cs += C;
-    if (p_cs >= p_nz1) {  // next tile
-      p_tile += gridDim.x;
-      if (p_tile < ntiles) {
-        const int64_t b0 = row0 + p_tile * kRows;
-        p_cs = row_ptr[b0];
-        p_nz1 = row_ptr[min(b0 + kRows, row1)];
-      }
+    p_cs += CW;
+    if (p_cs >= p_nz1) {  // every tile has >= 1 item, so empty rows still write 0
+      p_tile += nwarps;
+      p_cs = q_nz0;
+      p_nz1 = q_nz1;
+      if (p_tile + nwarps < ntiles) tile_nz(p_tile + nwarps, &q_nz0, &q_nz1);
     }
   };
-  if (tid == 0) {
+  if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (p_tile < ntiles) {
-      const int64_t b0 = row0 + p_tile * kRows;
-      p_cs = row_ptr[b0];
-      p_nz1 = row_ptr[min(b0 + kRows, row1)];
+    tile_nz(p_tile, &p_cs, &p_nz1);
+    if (p_tile + nwarps < ntiles) tile_nz(p_tile + nwarps, &q_nz0, &q_nz1);
 #pragma unroll
-      for (int s = 0; s < S; ++s)
-        if (p_tile < ntiles) p_issue(s);
-    }
+    for (int s = 0; s < S; ++s)
+      if (p_tile < ntiles) p_issue(s);
   }
-  __syncthreads();
+  __syncwarp();
 
+  // ---- consumers: this tile's row bounds + perm, next tile's prefetched
+  auto row_info = [&](int64_t t, int64_t* rs, int64_t* re, int64_t* pm) {
+    const int64_t r = row0 + t * 32 + lane;
+    if (r < row1) {
+      *rs = row_ptr[r];
+      *re = row_ptr[r + 1];
+      *pm = perm ? (int64_t)perm[r] : 0;
+    } else {
+      *rs = *re = *pm = 0;
+    }
+  };
+  int64_t rs, re, pm, nrs = 0, nre = 0, npm = 0;
+  row_info(first, &rs, &re, &pm);
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t b0 = row0 + tile * kRows;
-    const int64_t b1 = min(b0 + kRows, row1);
-    const int64_t r = b0 + tid;
-    const int64_t nz0 = row_ptr[b0], nz1 = row_ptr[b1];
-    int64_t rs = 0, re = 0;
-    if (r < b1) {
-      rs = row_ptr[r];
-      re = row_ptr[r + 1];
-    }
+  for (int64_t tile = first; tile < ntiles; tile += nwarps) {
+    if (tile + nwarps < ntiles) row_info(tile + nwarps, &nrs, &nre, &npm);
+    const int64_t r0 = row0 + tile * 32;
+    const int64_t nz0 = __shfl_sync(0xffffffffu, rs, 0);
+    const int64_t nz1 = __shfl_sync(0xffffffffu, re, (int)min((int64_t)31, row1 - 1 - r0));
     double acc = 0.0;
     int64_t cs = nz0;
     do {
-      const int n = (int)min((int64_t)C, nz1 - cs);
+      const int n = (int)min((int64_t)CW, nz1 - cs);
       mbar_wait(&full[stage], phase);
       const double* sv = sval(stage) + (((uintptr_t)(val + cs) & 15) >> 3);
       const int32_t* sc = scol(stage) + (((uintptr_t)(col + cs) & 15) >> 2);
-      constexpr int U = C / kRows;
-      int c[U];
+      const int a = (int)(max(rs, cs) - cs);
+      const int cnt = max((int)(min(re, cs + n) - cs) - a, 0);
+      const int m = __reduce_max_sync(0xffffffffu, cnt);
+      for (int j0 = 0; j0 < m; j0 += B) {
+        int c[B];
+        double g[B];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = tid + u * kRows;
-        c[u] = k < n ? sc[k] : 0;
-      }
-      double g[U];
+        for (int j = 0; j < B; ++j) c[j] = j0 + j < cnt ? sc[a + j0 + j] : 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = tid + u * kRows;
-        if (k < n) g[u] = ld_keep(x + c[u], keep);
-      }
+        for (int j = 0; j < B; ++j)
+          if (j0 + j < cnt) g[j] = ld_keep(x + c[j], keep);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = tid + u * kRows;
-        if (k < n) prod[swz(k)] = __dmul_rn(sv[k], g[u]);
+        for (int j = 0; j < B; ++j)
+          if (j0 + j < cnt) acc = __dadd_rn(acc, __dmul_rn(sv[a + j0 + j], g[j]));
       }
-      __syncthreads();
-      const int64_t a = max(rs, cs), b = min(re, cs + n);
-      for (int64_t k = a; k < b; ++k) acc = __dadd_rn(acc, prod[swz((int)(k - cs))]);
-      __syncthreads();  // stage and prod free
-      if (tid == 0 && p_tile < ntiles) {
+      __syncwarp();
+      if (lane == 0 && p_tile < ntiles) {  // stage consumed: refill it S items ahead
         fence_proxy_async_smem();
         p_issue(stage);
       }
@@ -311,12 +271,15 @@ __global__ void __launch_bounds__(kRows, MINB)
         stage = 0;
         phase ^= 1u;
       }
-      cs += C;
+      cs += CW;
     } while (cs < nz1);
-    if (r < b1) {
-      if (perm) y[(int64_t)perm[r]] = acc;
-      else y[r - row0] = acc;
+    if (r0 + lane < row1) {
+      if (perm) y[pm] = acc;
+      else y[r0 + lane - row0] = acc;
     }
+    rs = nrs;
+    re = nre;
+    pm = npm;
   }
 }
 
@@ -378,20 +341,34 @@ int spmv_variant() {
   return v;
 }
 
-template <typename Q, int C, int S, int MINB>
-int launch_bulk(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
-                int64_t row1, const void* pm, double* y, const DeviceInfo& di, cudaStream_t s) {
-  using L = BulkLayout<C, S>;
-  auto k = spmv_bulk_kernel<Q, C, S, MINB>;
+// Shared-memory carveout: just what the resident CTAs need.  The rest of the
+// unified 256 KB stays L1, which holds the in-flight x gathers — with less
+// than ~100 KB of L1 the SM's gather rate halves (scripts/micro/l2gather.cu:
+// 0.88 gathers/clk/SM at carveout <= 64 %, 0.44 at >= 86 %).
+inline int carveout_pct(size_t smem_per_sm) {
+  const size_t max_smem = 228 * 1024;
+  const int pct = (int)((smem_per_sm * 100 + max_smem - 1) / max_smem);
+  return pct > 100 ? 100 : pct;
+}
+
+template <typename Q, int CW, int S, int WARPS, int MINB, int B>
+int launch_lpr(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
+               int64_t row1, const void* pm, double* y, const DeviceInfo& di, cudaStream_t s) {
+  using L = LprLayout<CW, S, WARPS>;
+  auto k = spmv_lpr_kernel<Q, CW, S, WARPS, MINB, B>;
   HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes));
-  const int64_t ntiles = ceil_div(row1 - row0, kRows);
+  HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   carveout_pct(MINB * (L::kBytes + 256 + 1024))));
+  const int64_t ntiles = ceil_div(row1 - row0, 32);
   int64_t grid = (int64_t)di.sms * MINB;
-  if (grid > ntiles) grid = ntiles;
-  k<<<(unsigned)grid, kRows, L::kBytes, s>>>(reinterpret_cast<const int32_t*>(rp), reinterpret_cast<const int32_t*>(ci),
-                                             v, x, row0, row1, reinterpret_cast<const Q*>(pm), y, ntiles);
+  if (grid > ceil_div(ntiles, WARPS)) grid = ceil_div(ntiles, WARPS);
+  k<<<(unsigned)grid, 32 * WARPS, L::kBytes, s>>>(reinterpret_cast<const int32_t*>(rp), reinterpret_cast<const int32_t*>(ci),
+                                                  v, x, row0, row1, reinterpret_cast<const Q*>(pm), y, ntiles);
   return check_launch();
 }
 
+// HB_SPMV_CFG (experiments, scripts/sweep_spmv.sh): 0 default, 1 the generic
+// CTA-blocked kernel, 2.. alternative lane-per-row shapes <CW, S, WARPS, MINB, B>.
 template <typename P, typename C, typename Q>
 int launch_spmv(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
                 int64_t row1, const void* pm, double* y, int mode, cudaStream_t s) {
@@ -403,27 +380,25 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
   auto c = reinterpret_cast<const C*>(ci);
   auto q = reinterpret_cast<const Q*>(pm);
   const int var = spmv_variant();
-  if (mode == 0 && sizeof(P) == 4 && sizeof(C) == 4 && var >= 2 && var <= 6) {
-    switch (var) {
-      case 2: return launch_bulk<Q, 2048, 3, 2>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 3: return launch_bulk<Q, 2048, 2, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 4: return launch_bulk<Q, 1024, 4, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 5: return launch_bulk<Q, 4096, 2, 1>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      default: return launch_bulk<Q, 1024, 2, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
-    }
-  }
-  if (mode == 2 || (mode == 0 && var == 1)) {
-    const int64_t blocks = ceil_div(rows, 32 * kWarpsPerCta);
-    spmv_wseq_kernel<P, C, Q><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p, c, v, x, row0, row1, q, y);
-  } else if (mode == 1) {
+  if (mode == 1) {
     int64_t blocks = ceil_div(rows, 8);
     if (blocks > (int64_t)di.sms * 8) blocks = (int64_t)di.sms * 8;
     spmv_warp_kernel<P, C, Q><<<(int)blocks, 256, 0, s>>>(p, c, v, x, row0, row1, q, y);
-  } else {
-    const int64_t blocks = ceil_div(rows, kRows);
-    if (blocks > INT32_MAX) { set_error("too many rows"); return HB_EINVAL; }
-    spmv_seq_kernel<P, C, Q><<<(unsigned)blocks, kRows, 0, s>>>(p, c, v, x, row0, row1, q, y);
+    return check_launch();
   }
+  if (sizeof(P) == 4 && sizeof(C) == 4 && var != 1) {
+    switch (var) {
+      case 2: return launch_lpr<Q, 256, 2, 4, 4, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 3: return launch_lpr<Q, 256, 2, 8, 3, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 4: return launch_lpr<Q, 256, 2, 4, 6, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 5: return launch_lpr<Q, 256, 2, 4, 4, 8>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 6: return launch_lpr<Q, 192, 2, 4, 8, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      default: return launch_lpr<Q, 256, 2, 4, 6, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
+    }
+  }
+  const int64_t blocks = ceil_div(rows, kRows);
+  if (blocks > INT32_MAX) { set_error("too many rows"); return HB_EINVAL; }
+  spmv_seq_kernel<P, C, Q><<<(unsigned)blocks, kRows, 0, s>>>(p, c, v, x, row0, row1, q, y);
   return check_launch();
 }
 
@@ -432,6 +407,11 @@ int dispatch_perm(int perm_code, const void* rp, const void* ci, const double* v
                   int64_t row0, int64_t row1, const void* pm, double* y, int mode, cudaStream_t s) {
   if (perm_code == HB_I32) return launch_spmv<P, C, int32_t>(rp, ci, v, x, row0, row1, pm, y, mode, s);
   return launch_spmv<P, C, int64_t>(rp, ci, v, x, row0, row1, pm, y, mode, s);
+}
+
+__global__ void narrow_i64_kernel(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
 }
 
 int read_index(const void* p, int code, int64_t i, bool dev, cudaStream_t s, int64_t* out) {
@@ -487,22 +467,43 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
   HB_TRY(read_index(row_ptr, ptr_code, row1, false, s, &nz1));
   HB_CHECK_ARG(nz1 >= nz0 && nz0 >= 0, "row_ptr is not non-decreasing");
   DevBuf d_ptr, d_col, d_val, d_x, d_y;
-  // rebase row_ptr so the staged col/val slices start at 0
-  std::vector<int64_t> ptr_local((size_t)rows + 1);
+  // rebase row_ptr so the staged col/val slices start at 0; int32 when the
+  // range allows, so int32 col_idx takes the lane-per-row kernel
+  const bool p32 = nz1 - nz0 <= (int64_t)INT32_MAX;
+  std::vector<int64_t> ptr64(p32 ? 0 : (size_t)rows + 1);
+  std::vector<int32_t> ptr32(p32 ? (size_t)rows + 1 : 0);
   for (int64_t i = 0; i <= rows; ++i) {
     int64_t v;
     read_index(row_ptr, ptr_code, row0 + i, false, s, &v);
-    ptr_local[(size_t)i] = v - nz0;
+    if (p32) ptr32[(size_t)i] = (int32_t)(v - nz0);
+    else ptr64[(size_t)i] = v - nz0;
   }
   (void)pe;
-  HB_TRY(stage_in(&d_ptr, ptr_local.data(), ptr_local.size() * 8, false, s));
+  if (p32) HB_TRY(stage_in(&d_ptr, ptr32.data(), ptr32.size() * 4, false, s));
+  else HB_TRY(stage_in(&d_ptr, ptr64.data(), ptr64.size() * 8, false, s));
   HB_TRY(stage_in(&d_col, reinterpret_cast<const char*>(col_idx) + nz0 * ce, (size_t)(nz1 - nz0) * ce, false, s));
   HB_TRY(stage_in(&d_val, values + nz0, (size_t)(nz1 - nz0) * 8, false, s));
   HB_TRY(stage_in(&d_x, x, (size_t)cols * 8, false, s));
   HB_TRY(alloc(&d_y, (size_t)rows * 8, s));
-  int rc = col_code == HB_I32
-               ? launch_spmv<int64_t, int32_t, int64_t>(d_ptr.ptr, d_col.ptr, d_val.as<double>(), d_x.as<double>(), 0, rows, nullptr, d_y.as<double>(), mode, s)
-               : launch_spmv<int64_t, int64_t, int64_t>(d_ptr.ptr, d_col.ptr, d_val.as<double>(), d_x.as<double>(), 0, rows, nullptr, d_y.as<double>(), mode, s);
+  const double* dv = d_val.as<double>();
+  const double* dx = d_x.as<double>();
+  double* dy = d_y.as<double>();
+  int rc;
+  DevBuf d_col32;
+  if (p32 && col_code == HB_I64 && cols <= (int64_t)INT32_MAX && nz1 > nz0) {
+    // int64 host columns: narrow on the device so the lane-per-row kernel runs
+    HB_TRY(alloc(&d_col32, (size_t)(nz1 - nz0) * 4, s));
+    DeviceInfo di;
+    HB_TRY(device_info(&di));
+    int64_t g = ceil_div(nz1 - nz0, 256);
+    if (g > (int64_t)di.sms * 16) g = (int64_t)di.sms * 16;
+    narrow_i64_kernel<<<(int)g, 256, 0, s>>>(d_col.as<int64_t>(), nz1 - nz0, d_col32.as<int32_t>());
+    HB_TRY(check_launch());
+    rc = launch_spmv<int32_t, int32_t, int64_t>(d_ptr.ptr, d_col32.ptr, dv, dx, 0, rows, nullptr, dy, mode, s);
+  } else if (p32) rc = col_code == HB_I32 ? launch_spmv<int32_t, int32_t, int64_t>(d_ptr.ptr, d_col.ptr, dv, dx, 0, rows, nullptr, dy, mode, s)
+                                   : launch_spmv<int32_t, int64_t, int64_t>(d_ptr.ptr, d_col.ptr, dv, dx, 0, rows, nullptr, dy, mode, s);
+  else rc = col_code == HB_I32 ? launch_spmv<int64_t, int32_t, int64_t>(d_ptr.ptr, d_col.ptr, dv, dx, 0, rows, nullptr, dy, mode, s)
+                               : launch_spmv<int64_t, int64_t, int64_t>(d_ptr.ptr, d_col.ptr, dv, dx, 0, rows, nullptr, dy, mode, s);
   if (rc != HB_OK) return rc;
   if (perm == nullptr) {
     HB_CUDA_TRY(cudaMemcpyAsync(y, d_y.ptr, (size_t)rows * 8, cudaMemcpyDeviceToHost, s));

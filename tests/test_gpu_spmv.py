@@ -71,7 +71,8 @@ def test_kats_identity_zero_and_mismatch(platform13):
         spmv_hybrid(prep, np.ones(4))
 
 
-def test_long_and_empty_rows_bit_exact():
+@pytest.mark.parametrize("idx", [np.int32, np.int64])
+def test_long_and_empty_rows_bit_exact(idx):
     # rows far longer than one staged chunk, interleaved with empty rows
     rng = np.random.default_rng(3)
     lens = np.array([0, 5, 0, 9000, 1, 0, 20000, 3, 0, 0, 4097, 4096, 4095, 17])
@@ -84,13 +85,37 @@ def test_long_and_empty_rows_bit_exact():
     m = CsrMatrix(rows, cols, ptr, col, val)
     want = ospmv.sequential_rows(ptr, col, val, x)
     assert np.array_equal(bits(gpu_spmv(m, x, 0, rows)), bits(want))
-    md = m.to_device(np.int64)
+    md = m.to_device(idx)
     import torch
 
     got = gpu_spmv(md, torch.from_numpy(x).cuda(), 0, rows)
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
     got = gpu_spmv(md, torch.from_numpy(x).cuda(), 2, 9)
     assert np.array_equal(bits(got.cpu().numpy()), bits(want[2:9]))
+
+
+def test_int32_row_ranges_and_unaligned_views_bit_exact():
+    # lane-per-row kernel: many tiles, row ranges that start/end inside a tile,
+    # and col/val views whose first element is not 16-byte aligned
+    import torch
+
+    ptr, col, val = ods.csr(30_011, 30_011, 7, 6e-4)
+    x = 2.0 * orng.uniform_floats(orng.mix_seed(7, 0xDEC0), 30_011) - 1.0
+    want = ospmv.sequential_rows(ptr, col, val, x)
+    m = CsrMatrix(30_011, 30_011, ptr, col, val)
+    md = m.to_device(np.int32)
+    xd = torch.from_numpy(x).cuda()
+    for r0, r1 in [(0, 30_011), (1, 30_011), (5, 37), (31, 33), (12_345, 29_999), (30_010, 30_011)]:
+        got = gpu_spmv(md, xd, r0, r1)
+        assert np.array_equal(bits(got.cpu().numpy()), bits(want[r0:r1])), (r0, r1)
+    # views offset by 1..3 elements: the bulk copies start mid 16-byte block
+    pt = torch.from_numpy(ptr.astype(np.int32)).cuda()
+    for shift in (1, 2, 3):
+        ct = torch.cat([torch.zeros(shift, dtype=torch.int32), torch.from_numpy(col.astype(np.int32))]).cuda()[shift:]
+        vt = torch.cat([torch.zeros(shift, dtype=torch.float64), torch.from_numpy(val)]).cuda()[shift:]
+        assert ct.data_ptr() % 16 != 0 or vt.data_ptr() % 16 != 0
+        got = gpu_spmv(CsrMatrix(30_011, 30_011, pt, ct, vt), xd, 0, 30_011)
+        assert np.array_equal(bits(got.cpu().numpy()), bits(want)), shift
 
 
 def test_warp_mode_within_tolerance():

@@ -53,6 +53,7 @@ extern "C" {
 #define HB_I32 6
 #define HB_U64 7
 #define HB_I64 8
+#define HB_F64 9
 
 /* ------------------------------------------------------------------ runtime */
 int hb_version(void);
@@ -137,6 +138,18 @@ int hb_csr_validate(const void* row_ptr, int ptr_code, const void* col_idx, int 
 int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t radius,
                     const double* spatial, const double* range256, int32_t row0, int32_t row1,
                     void* out, int out_code, int flags, void* stream);
+
+/* -------------------------------------------------------------- convolution
+ * Replaces convolve_rows / ConvolutionWorkload.run_part
+ * (kernels_regular.py:359-414): output rows [row0, row1) of the clamp-to-edge
+ * correlation of img[height][width] (in_code HB_U8 or HB_F64) with the
+ * (2r+1)^2 row-major weights.  Bit-identical to the reference for fp64 output
+ * (out_code 64): taps in row-major order, zero weights skipped, rounded fp64
+ * multiply then add, no FMA.  out_code 32 rounds that result to fp32.
+ * Host-pointer calls stage only the strip plus its clamped halo rows.     */
+int hb_convolve(const void* img, int in_code, int32_t height, int32_t width, int32_t radius,
+                const double* weights, int32_t row0, int32_t row1, void* out, int out_code,
+                int flags, void* stream);
 
 /* --------------------------------------------------------------------- sort
  * Replaces the DeviceB side of sample_sort_hybrid (kernels_regular.py:239-310)

@@ -29,7 +29,7 @@ HB_GEN_RAW, HB_GEN_LOW8, HB_GEN_HI32, HB_GEN_MOD = range(4)
 HB_SPMV_SEQ, HB_SPMV_WARP = 0, 1
 
 # numpy dtype.str (sans byte order) -> element code of include/hb200.h
-DTYPE_CODES = {"u1": 1, "i1": 2, "u2": 3, "i2": 4, "u4": 5, "i4": 6, "u8": 7, "i8": 8}
+DTYPE_CODES = {"u1": 1, "i1": 2, "u2": 3, "i2": 4, "u4": 5, "i4": 6, "u8": 7, "i8": 8, "f8": 9}
 
 _c = ctypes
 _vp, _i32, _i64, _u64 = _c.c_void_p, _c.c_int32, _c.c_int64, _c.c_uint64
@@ -48,6 +48,7 @@ _SIGNATURES: dict[str, list] = {
     "hb_csr_validate": [_vp, _int, _vp, _int, _i64, _i64, _i64, _vp, _int, _vp],
     "hb_spmv_preprocess": [_vp, _int, _vp, _int, _vp, _i64, _vp, _int, _vp, _vp, _vp, _int, _vp],
     "hb_bilateral_u8": [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _int, _int, _vp],
+    "hb_convolve": [_vp, _int, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _int, _int, _vp],
     "hb_sort": [_vp, _vp, _int, _vp, _vp, _i64, _vp, _int, _vp],
     "hb_sort_bounds": [_vp, _int, _vp, _i64, _vp, _vp, _i32, _vp, _int, _vp],
     "hb_list_rank": [_vp, _int, _i64, _i64, _vp, _int, _vp],

@@ -1,0 +1,183 @@
+// conv.cu — clamp-to-edge 2-D correlation on row strips (replaces
+// convolve_rows / ConvolutionWorkload.run_part, reference
+// kernels_regular.py:359-414).
+//
+// Arithmetic is the reference's, bit for bit: the reference adds one weighted
+// plane per tap, `out += weight * slab[dy:, dx:]`, in row-major (dy, dx)
+// order, skipping taps whose weight is exactly 0.0 (:376-381).  Per pixel
+// that is acc = acc + w*I with a rounded fp64 multiply and a rounded add (no
+// FMA), acc starting at +0.0, the pixel converted to fp64 exactly
+// (`pixels.astype(np.float64)`).  Zero taps are skipped here too, so -0.0,
+// inf and NaN propagate exactly as in the reference.
+//
+// Layout: one CTA = a 32 x 64 output tile; the clamped (32+2R) x (64+2R)
+// halo tile is staged in shared memory as fp64 (uint8 or fp64 input); each
+// thread owns 8 horizontally adjacent outputs and holds the (8+2R)-wide row
+// segment of the current tap row in registers, so each tap costs one DMUL +
+// one DADD per pixel and no shared-memory traffic (the weight is a warp-wide
+// broadcast).  Bound: fp64 issue (2 flops per tap per pixel), not HBM.
+#include "common.cuh"
+
+namespace hb {
+namespace {
+
+constexpr int kTileH = 32;
+constexpr int kTileW = 64;
+constexpr int kPx = 8;
+constexpr int kThreads = kTileH * kTileW / kPx;  // 256
+constexpr int kMaxR = 8;
+
+template <typename IN>
+__device__ __forceinline__ double to_f64(IN v) { return (double)v; }
+
+template <int R, typename IN, typename OUT>
+__global__ void __launch_bounds__(kThreads, 2)
+    conv_tile_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
+                     const double* __restrict__ weights, OUT* __restrict__ out) {
+  constexpr int S = 2 * R + 1;
+  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sw = reinterpret_cast<double*>(smem);  // [S*S]
+  double* tile = sw + S * S;                     // [TH][TW]
+  const int tid = threadIdx.x;
+  const int y0 = row0 + blockIdx.y * kTileH;
+  const int x0 = blockIdx.x * kTileW;
+  for (int i = tid; i < S * S; i += kThreads) sw[i] = weights[i];
+  for (int i = tid; i < TH * TW; i += kThreads) {
+    const int ty = i / TW, tx = i - ty * TW;
+    const int gy = min(max(y0 - R + ty, 0), H - 1);
+    const int gx = min(max(x0 - R + tx, 0), W - 1);
+    tile[i] = to_f64(img[(int64_t)gy * W + gx]);
+  }
+  __syncthreads();
+  const int py = tid / (kTileW / kPx);
+  const int px = (tid % (kTileW / kPx)) * kPx;
+  const int gy = y0 + py;
+  if (gy >= row1) return;
+  double acc[kPx];
+#pragma unroll
+  for (int j = 0; j < kPx; ++j) acc[j] = 0.0;
+#pragma unroll 1
+  for (int dy = 0; dy < S; ++dy) {
+    double seg[kPx + 2 * R];
+    const double* trow = tile + (py + dy) * TW + px;
+#pragma unroll
+    for (int k = 0; k < kPx + 2 * R; ++k) seg[k] = trow[k];
+#pragma unroll
+    for (int dx = 0; dx < S; ++dx) {
+      const double w = sw[dy * S + dx];
+      if (w != 0.0) {
+#pragma unroll
+        for (int j = 0; j < kPx; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(w, seg[j + dx]));
+      }
+    }
+  }
+  OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
+#pragma unroll
+  for (int j = 0; j < kPx; ++j)
+    if (x0 + px + j < W) o[j] = (OUT)acc[j];
+}
+
+// radius > kMaxR: same arithmetic, neighbours read from global memory
+template <typename IN, typename OUT>
+__global__ void conv_generic_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1, int R,
+                                    const double* __restrict__ weights, OUT* __restrict__ out) {
+  const int64_t n = (int64_t)(row1 - row0) * W;
+  const int S = 2 * R + 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = row0 + (int)(i / W), x = (int)(i % W);
+    double acc = 0.0;
+    for (int dy = 0; dy < S; ++dy) {
+      const int yy = min(max(y + dy - R, 0), H - 1);
+      for (int dx = 0; dx < S; ++dx) {
+        const double w = weights[dy * S + dx];
+        if (w == 0.0) continue;
+        const int xx = min(max(x + dx - R, 0), W - 1);
+        acc = __dadd_rn(acc, __dmul_rn(w, to_f64(img[(int64_t)yy * W + xx])));
+      }
+    }
+    out[i] = (OUT)acc;
+  }
+}
+
+template <int R, typename IN, typename OUT>
+int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w, OUT* out, cudaStream_t s) {
+  constexpr int S = 2 * R + 1;
+  const size_t smem = (size_t)S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 8;
+  HB_CUDA_TRY(cudaFuncSetAttribute(conv_tile_kernel<R, IN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
+  conv_tile_kernel<R, IN, OUT><<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, w, out);
+  return check_launch();
+}
+
+template <typename IN, typename OUT>
+int launch_conv(const IN* img, int H, int W, int row0, int row1, int R, const double* w, OUT* out, cudaStream_t s) {
+  switch (R) {
+    case 0: return launch_tile<0, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 1: return launch_tile<1, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 2: return launch_tile<2, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 3: return launch_tile<3, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 4: return launch_tile<4, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 5: return launch_tile<5, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 6: return launch_tile<6, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 7: return launch_tile<7, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 8: return launch_tile<8, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    default: {
+      DeviceInfo di;
+      HB_TRY(device_info(&di));
+      int64_t blocks = ceil_div((int64_t)(row1 - row0) * W, 256);
+      if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+      conv_generic_kernel<IN, OUT><<<(int)blocks, 256, 0, s>>>(img, H, W, row0, row1, R, w, out);
+      return check_launch();
+    }
+  }
+}
+
+template <typename IN>
+int dispatch_out(const void* img, int H, int W, int row0, int row1, int R, const double* w, void* out,
+                 int out_code, cudaStream_t s) {
+  auto in = reinterpret_cast<const IN*>(img);
+  return out_code == 64 ? launch_conv<IN, double>(in, H, W, row0, row1, R, w, reinterpret_cast<double*>(out), s)
+                        : launch_conv<IN, float>(in, H, W, row0, row1, R, w, reinterpret_cast<float*>(out), s);
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t width, int32_t radius,
+                           const double* weights, int32_t row0, int32_t row1, void* out, int out_code,
+                           int flags, void* stream) {
+  HB_CHECK_ARG(height > 0 && width > 0, "image must be non-empty");
+  HB_CHECK_ARG(radius >= 0 && radius <= 255, "radius must be in [0, 255]");
+  HB_CHECK_ARG(row0 >= 0 && row1 >= row0 && row1 <= height, "bad row range");
+  HB_CHECK_ARG(in_code == HB_U8 || in_code == HB_F64, "image must be uint8 or float64");
+  HB_CHECK_ARG(out_code == 64 || out_code == 32, "out_code must be 64 (fp64) or 32 (fp32)");
+  if (row1 == row0) return HB_OK;
+  HB_CHECK_ARG(img && weights && out, "NULL pointer");
+  const bool dev = flags & HB_DEVICE_PTRS;
+  HB_CHECK_ARG(dev || !(flags & HB_ASYNC), "HB_ASYNC requires device pointers");
+  cudaStream_t s = as_stream(stream);
+  const int S = 2 * radius + 1;
+  const size_t es_in = in_code == HB_U8 ? 1 : 8;
+  // host calls stage only the strip and its clamped halo rows
+  int in0 = 0, in1 = height;
+  if (!dev) {
+    in0 = row0 - radius < 0 ? 0 : row0 - radius;
+    in1 = row1 + radius > height ? height : row1 + radius;
+  }
+  DevBuf d_img, d_w, d_out;
+  const char* src = reinterpret_cast<const char*>(img) + (dev ? 0 : (size_t)in0 * width * es_in);
+  HB_TRY(stage_in(&d_img, src, (size_t)(in1 - in0) * width * es_in, dev, s));
+  HB_TRY(stage_in(&d_w, weights, (size_t)S * S * 8, dev, s));
+  const size_t out_bytes = (size_t)(row1 - row0) * width * (out_code == 64 ? 8 : 4);
+  HB_TRY(stage_out(&d_out, out, out_bytes, dev, s));
+  const int h = in1 - in0, r0 = row0 - in0, r1 = row1 - in0;
+  const int rc = in_code == HB_U8
+                     ? dispatch_out<uint8_t>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), d_out.ptr, out_code, s)
+                     : dispatch_out<double>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), d_out.ptr, out_code, s);
+  if (rc != HB_OK) return rc;
+  HB_TRY(copy_out(out, d_out, out_bytes, dev, s));
+  return finish(flags, s);
+}

@@ -1,5 +1,6 @@
 """Regular hot-path kernels behind the reference's own entry points
-(hybridbench/kernels_regular.py): histogram, sort, bilateral filter.
+(hybridbench/kernels_regular.py): histogram, sort, convolution, bilateral
+filter.
 
 Each workload keeps the reference's Partitionable protocol and names.
 `run_part(DeviceA, …)` computes the host share with numpy on the host
@@ -79,7 +80,7 @@ def gpu_histogram(part: Any, bin_count: int, out: Any = None, *, asynchronous: b
     if b.size or b.device:
         require_gpu()
     _lib.load()
-    if b.code == 0:
+    if b.code == 0 or b.dtype.kind == "f":
         raise TypeError(f"histogram input must be an integer array, got {b.dtype}")
     if b.device:
         import torch
@@ -301,6 +302,147 @@ def hybrid_sort(data: Any, platform: Platform, leaf_a: int = 2048, leaf_b: int =
     """kernels_regular.py:313-321."""
     out, _, _ = sample_sort_hybrid(data, platform, leaf_a, leaf_b, share)
     return out
+
+
+# --------------------------------------------------------------------------
+# convolution (kernels_regular.py:327-414)
+
+
+@dataclass(frozen=True)
+class FilterKernel:
+    """Square odd-sided weight stencil (kernels_regular.py:327-356)."""
+
+    weights: np.ndarray
+
+    def __post_init__(self) -> None:
+        w = np.asarray(self.weights)
+        if w.ndim != 2 or w.shape[0] != w.shape[1] or w.shape[0] % 2 == 0:
+            raise ValueError("kernel must be square with odd side")
+        if not np.isfinite(w).all():
+            raise ValueError("kernel weights must be finite")
+
+    @property
+    def radius(self) -> int:
+        return self.weights.shape[0] // 2
+
+    @classmethod
+    def delta(cls, radius: int) -> "FilterKernel":
+        w = np.zeros((2 * radius + 1, 2 * radius + 1))
+        w[radius, radius] = 1.0
+        return cls(w)
+
+    @classmethod
+    def gaussian(cls, radius: int, sigma: float | None = None) -> "FilterKernel":
+        sigma = sigma or max(radius / 2.0, 0.5)
+        ax = np.arange(-radius, radius + 1, dtype=np.float64)
+        g = np.exp(-(ax[:, None] ** 2 + ax[None, :] ** 2) / (2.0 * sigma**2))
+        return cls(g / g.sum())
+
+
+def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int) -> np.ndarray:
+    """Host (DeviceA) body, the reference arithmetic (:359-381): correlation of
+    rows [row0, row1) with clamp-to-edge borders, one weighted plane added per
+    non-zero tap in row-major order."""
+    pixels = to_host(pixels)
+    height, width = pixels.shape
+    r = kernel.radius
+    n_rows = row1 - row0
+    if n_rows <= 0:
+        return np.zeros((0, width))
+    rows_idx = np.clip(np.arange(row0 - r, row1 + r), 0, height - 1)
+    slab = np.pad(pixels[rows_idx].astype(np.float64), ((0, 0), (r, r)), mode="edge")
+    out = np.zeros((n_rows, width))
+    for dy in range(2 * r + 1):
+        for dx in range(2 * r + 1):
+            weight = kernel.weights[dy, dx]
+            if weight == 0.0:
+                continue
+            out += weight * slab[dy : dy + n_rows, dx : dx + width]
+    return out
+
+
+def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, out: Any = None,
+                      *, out_dtype: Any = np.float64, asynchronous: bool = False) -> Any:
+    """DeviceB body (hb_convolve): rows [row0, row1) on the GPU, bit-identical
+    to `convolve_rows` for fp64 output.  uint8 and float64 pixels go to the
+    kernel as they are; other dtypes are widened to float64 first (exactly
+    what `astype(np.float64)` does in the reference).  Host pixels → numpy
+    result; CUDA pixels → result tensor."""
+    _lib.load()
+    code = 64 if np.dtype(out_dtype) == np.float64 else 32
+    height, width = int(pixels.shape[0]), int(pixels.shape[1])
+    if not 0 <= row0 <= row1 <= height:
+        raise ValueError("bad row range")
+    if row1 > row0:
+        require_gpu()
+    w = np.ascontiguousarray(kernel.weights, dtype=np.float64)
+    if is_device_array(pixels):
+        import torch
+
+        if pixels.dtype not in (torch.uint8, torch.float64):
+            pixels = pixels.to(torch.float64)
+        pixels = pixels.contiguous()
+        tdt = torch.float64 if code == 64 else torch.float32
+        if out is None:
+            out = torch.empty((row1 - row0, width), dtype=tdt, device=pixels.device)
+        if row1 == row0:
+            return out
+        wt = torch.from_numpy(w).to(pixels.device)
+        in_code = _lib.DTYPE_CODES["u1" if pixels.dtype == torch.uint8 else "f8"]
+        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0)
+        _lib.call("hb_convolve", vp(pixels.data_ptr()), in_code, height, width, kernel.radius, vp(wt.data_ptr()),
+                  row0, row1, vp(out.data_ptr()), code, flags, current_stream_handle(pixels))
+        return out
+    arr = np.asarray(pixels)
+    if arr.dtype not in (np.uint8, np.float64):
+        arr = arr.astype(np.float64)
+    img = buf(arr)
+    if out is None:
+        out = np.empty((row1 - row0, width), dtype=np.float64 if code == 64 else np.float32)
+    if row1 == row0:
+        return out
+    _lib.call("hb_convolve", vp(img.ptr), img.code, height, width, kernel.radius, vp(w.ctypes.data),
+              row0, row1, vp(out.ctypes.data), code, 0, current_stream_handle())
+    return out
+
+
+class ConvolutionWorkload:
+    """Horizontal strip split at floor(f·H); halo rows are read from the
+    shared source image (kernels_regular.py:384-405).  DeviceA: numpy planes;
+    DeviceB: the GPU tile kernel over the GPU group (floor(k·n/G) strips)."""
+
+    name = "conv"
+    unit = "neighbor accumulations"
+
+    def __init__(self, image: Image, kernel: FilterKernel):
+        self.image = image
+        self.kernel = kernel
+        self._per_row = image.width * (2 * kernel.radius + 1) ** 2
+
+    def partition(self, fraction_a: float):
+        split = int(math.floor(fraction_a * self.image.height))
+        return (0, split), (split, self.image.height)
+
+    def work_units(self, part) -> float:
+        return float((part[1] - part[0]) * self._per_row)
+
+    def run_part(self, device: Device, part) -> np.ndarray:
+        if device.id is DeviceId.B:
+            return sharding.run_sharded_rows(
+                part[0], part[1], lambda a, b: gpu_convolve_rows(self.image.pixels, self.kernel, a, b)
+            )
+        return convolve_rows(self.image.pixels, self.kernel, part[0], part[1])
+
+    def merge(self, partials: Sequence[np.ndarray]) -> Image:
+        return Image(np.vstack([sharding.to_numpy(p) for p in partials]))
+
+
+def hybrid_convolve(image: Image, kernel: FilterKernel, platform: Platform,
+                    share: WorkShare | None = None) -> Image:
+    """kernels_regular.py:408-414."""
+    workload = ConvolutionWorkload(image, kernel)
+    result, _ = run_workshared(platform, workload, share or formula_share(platform), baselines=False)
+    return result
 
 
 # --------------------------------------------------------------------------

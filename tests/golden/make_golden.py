@@ -15,8 +15,11 @@ REF = Path("/root/reference/pkg/src")
 OUT = Path(__file__).resolve().parent
 
 
-def main() -> None:
+def main(only: str | None = None) -> None:
     sys.path.insert(0, str(REF))
+    if only == "conv":
+        conv()
+        return
     from hybridbench import datasets, rng
     from hybridbench.kernels_irregular import (
         CsrMatrix,
@@ -120,8 +123,46 @@ def main() -> None:
         lr[f"stats_{i}"] = np.array([st.fis_rounds, st.reduced_size, st.removed_total, st.sublist_count])
         lr[f"sizes_{i}"] = np.array(st.round_sizes, dtype=np.int64)
     np.savez_compressed(OUT / "listrank.npz", **lr)
+    conv()
     print("golden fixtures written to", OUT)
 
 
+def conv() -> None:
+    """Convolution fixtures (kernels_regular.py:327-414): hybrid_convolve at
+    several shares, uint8 and float64 images, kernels with zero taps."""
+    from hybridbench import datasets, rng
+    from hybridbench.kernels_regular import ConvolutionWorkload, FilterKernel, Image, convolve_rows, hybrid_convolve
+    from hybridbench.platform import Platform
+    from hybridbench.worksharing import WorkShare
+
+    p13 = Platform.build(1.0, 3.0)
+    c = {}
+    rand5 = rng.uniform_floats(123, 25).reshape(5, 5) * 2 - 1
+    rand5[1, 3] = 0.0
+    rand5[4, 0] = 0.0
+    sparse7 = np.zeros((15, 15))
+    sparse7[::3, ::2] = rng.uniform_floats(77, 40).reshape(5, 8) - 0.5
+    cases = [(24, 9, rand5), (64, 4, FilterKernel.gaussian(3).weights), (40, 42, FilterKernel.delta(2).weights),
+             (37, 7, sparse7), (50, 1, FilterKernel.gaussian(7).weights), (30, 5, FilterKernel.gaussian(10).weights)]
+    for i, (side, seed, w) in enumerate(cases):
+        img = datasets.gen_image(side, seed)
+        k = FilterKernel(np.asarray(w, dtype=np.float64))
+        c[f"img_{i}"], c[f"w_{i}"] = img.pixels, k.weights
+        c[f"out_{i}"] = np.stack([hybrid_convolve(img, k, p13, WorkShare.manual(s)).pixels for s in (0.0, 0.3, 1.0)])
+        c[f"strip_{i}"] = convolve_rows(img.pixels, k, side // 3, side // 3 + 5)
+    # float64 image (linearity test input of test_kernels_regular.py:159-168)
+    a = datasets.gen_image(16, 1).pixels.astype(np.float64)
+    b = datasets.gen_image(16, 2).pixels.astype(np.float64)
+    f = 0.7 * a - 1.3 * b
+    k = FilterKernel.gaussian(2)
+    c["f64_img"], c["f64_w"], c["f64_out"] = f, k.weights, hybrid_convolve(Image(f), k, p13).pixels
+    # rectangular image, criterion-7 partition
+    rect = datasets.gen_image(48, 3).pixels[:20, :].copy()
+    c["rect_img"], c["rect_out"] = rect, hybrid_convolve(Image(rect), FilterKernel.gaussian(2), p13).pixels
+    wl = ConvolutionWorkload(Image(np.zeros((3600, 3600), dtype=np.uint8)), FilterKernel.delta(7))
+    c["part_18"] = np.array(wl.partition(0.18))
+    np.savez_compressed(OUT / "conv.npz", **c)
+
+
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

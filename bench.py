@@ -36,6 +36,7 @@ sys.path.insert(0, str(ROOT))
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
+FP64_PEAK_GFLOPS = 18370.0  # non-FMA fp64 instructions/s, scripts/micro/fp64peak.cu
 METRIC = "per-workload throughput (SpMV GFLOP/s, sort Mkeys/s) and HBM-roofline fraction"
 
 
@@ -438,6 +439,63 @@ class BilatBench:
         return 2
 
 
+class ConvBench(BilatBench):
+    """Convolution (not a BASELINE config): 16384 x 16384 uint8
+    image, 15 x 15 Gaussian (the paper's figure kernel, FilterKernel.gaussian(7)),
+    fp64 arithmetic bit-identical to the reference, fp32 output image."""
+
+    name = "conv"
+    kernel = "conv_tile_kernel"
+    compute_bound = "fp64 issue (1 DMUL + 1 DADD per tap)"
+
+    def __init__(self, side: int = 16384, radius: int = 7, seed: int = 42):
+        super().__init__(side, radius, seed)
+
+    def config(self):
+        return {"workload": f"conv: {self.side}x{self.side} image, {2 * self.radius + 1}x{2 * self.radius + 1} Gaussian, fp64 taps, fp32 out",
+                "side": self.side, "radius": self.radius, "seed": self.seed,
+                "input": "gen_image(16384, 42) (splitmix64 low byte, device-generated)",
+                "l2": "input 256 MiB + output 1 GiB > L2"}
+
+    def setup(self, rank, world):
+        super().setup(rank, world)
+        from paper_1303_2171_b200.kernels_regular import FilterKernel
+
+        self.fk = FilterKernel.gaussian(self.radius)
+
+    def step(self):
+        from paper_1303_2171_b200.kernels_regular import gpu_convolve_rows
+
+        gpu_convolve_rows(self.img, self.fk, 0, self.side, out=self.out, out_dtype=np.float32, asynchronous=True)
+        return 1
+
+    def flops_per_launch(self):
+        return self.side * self.side * (2 * self.radius + 1) ** 2 * 2
+
+    def verify(self):
+        from oracle import conv as oconv
+
+        host = self.img.cpu().numpy()
+        ok = True
+        for a, b in [(0, 8), (8000, 8008), (self.side - 8, self.side)]:
+            want = oconv.rows(host, self.fk.weights, a, b).astype(np.float32)
+            ok &= np.array_equal(self.out[a:b].cpu().numpy(), want)
+        return bool(ok)
+
+    def e2e_step(self):
+        from paper_1303_2171_b200.kernels_regular import hybrid_convolve
+
+        return hybrid_convolve(self.image, self.fk, self.platform, self.share)
+
+    def cpu_sample(self, budget_s: float):
+        from oracle import conv as oconv
+
+        rows = 128
+        host = self.img[: rows + self.radius].cpu().numpy()
+        fn = lambda: oconv.hybrid(host[:rows], self.fk.weights, 0.25)  # noqa: E731
+        return fn, rows * self.side, f"{rows} x {self.side} strip of the same image, formula share 0.25, 2 threads"
+
+
 class SortBench:
     """BASELINE configs[2]: LSD radix sort of 2^28 uint32 keys + uint32
     payload (gen_sort_data keys, payload = global index), per GPU;
@@ -445,7 +503,7 @@ class SortBench:
 
     name = "sort"
     unit = "Mkeys/s"
-    kernel = "onesweep_kernel"
+    kernel = "onesweep_ec_kernel"
 
     def __init__(self, n: int = 1 << 28, seed: int = 42):
         self.n, self.seed = n, seed
@@ -641,7 +699,7 @@ class LrBench:
         return 1
 
 
-WORKLOADS = {"hist": HistBench, "spmv": SpmvBench, "bilat": BilatBench, "sort": SortBench, "lr": LrBench}
+WORKLOADS = {"hist": HistBench, "spmv": SpmvBench, "bilat": BilatBench, "conv": ConvBench, "sort": SortBench, "lr": LrBench}
 
 
 # ---------------------------------------------------------------- drivers
@@ -779,9 +837,13 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
     }
     if hasattr(wl, "flops_per_launch"):
         # compute-bound kernel: fp64 issue is the bound, HBM fraction is low by design
+        ach = wl.flops_per_launch() / (ms / 1e3) / 1e9
         res["roofline"]["compute"] = {
-            "bound": "fp64 issue (2 DMUL + 2 DADD per tap)",
-            "achieved_gflops": wl.flops_per_launch() / (ms / 1e3) / 1e9,
+            "bound": getattr(wl, "compute_bound", "fp64 issue (2 DMUL + 2 DADD per tap)"),
+            "achieved_gflops": ach,
+            "peak_gflops": FP64_PEAK_GFLOPS,
+            "frac": ach / FP64_PEAK_GFLOPS,
+            "peak_source": "measured: scripts/micro/fp64peak.cu, DADD/DMUL 18.37 T instr/s on B200 (1 flop each, no FMA)",
             "flops_per_launch": wl.flops_per_launch(),
         }
     if with_cpu and rank == 0:

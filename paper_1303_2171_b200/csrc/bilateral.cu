@@ -15,6 +15,8 @@
 // one input row segment (PX+2R values, converted to fp64 once) in registers
 // while it sweeps the 2R+1 taps of that row, so shared-memory traffic per tap
 // is one range-table load.  The bound is fp64 issue (2 DMUL + 2 DADD per tap).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace hb {
@@ -26,24 +28,28 @@ constexpr int kPx = 8;                        // pixels per thread (one row segm
 constexpr int kThreads = kTileH * kTileW / kPx;  // 256
 constexpr int kMaxR = 8;
 
-template <int R, typename OUT>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int R, typename OUT, int STRIPE = 32, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB)
     bilateral_tile_kernel(const uint8_t* __restrict__ img, int H, int W, int row0, int row1,
                           const double* __restrict__ spatial, const double* __restrict__ range,
                           OUT* __restrict__ out) {
   constexpr int S = 2 * R + 1;
   constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* rng = reinterpret_cast<double*>(smem);            // [256][32] lane-striped
-  double* sp = rng + 256 * 32;                              // [S*S]
+  // range table striped over STRIPE lanes: entry e of lane l at [e][l % STRIPE];
+  // 8-byte loads are served per half-warp, so 16 stripes are already
+  // conflict-free and halve the table (32 KB)
+  constexpr int SH = STRIPE == 32 ? 5 : 4;
+  double* rng = reinterpret_cast<double*>(smem);            // [256][STRIPE]
+  double* sp = rng + 256 * STRIPE;                          // [S*S]
   int* tile = reinterpret_cast<int*>(sp + S * S);           // [TH][TW]
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  const int lane = tid & (STRIPE - 1);
   const int y0 = row0 + blockIdx.y * kTileH;  // first output row of the tile
   const int x0 = blockIdx.x * kTileW;
 
-  for (int i = tid; i < 256 * 32; i += kThreads) rng[i] = range[i >> 5];
+  for (int i = tid; i < 256 * STRIPE; i += kThreads) rng[i] = range[i >> SH];
   for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
   for (int i = tid; i < TH * TW; i += kThreads) {
     const int ty = i / TW, tx = i - ty * TW;
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int j = 0; j < kPx; ++j) {
         const int d = abs(nb[j + dx] - c[j]);
-        const double w = __dmul_rn(s, lane_rng[d << 5]);
+        const double w = __dmul_rn(s, lane_rng[d << SH]);
         num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
         den[j] = __dadd_rn(den[j], w);
       }
@@ -92,6 +98,105 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
   for (int j = 0; j < kPx; ++j)
     if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
+}
+
+// Persistent variant (HB_BILAT_CFG=3; measured no faster than one CTA per
+// tile, kept for the record): grid = 2 CTAs per SM, each CTA walks
+// tiles round-robin.  The lane-striped range table is built once per CTA
+// (not once per tile), and the halo of the NEXT tile is loaded into
+// registers before the current tile is filtered and written to the other
+// shared-memory buffer afterwards, so the global-load latency of the halo
+// is hidden behind the fp64 work instead of stalling every tile.
+template <int R, typename OUT>
+__global__ void __launch_bounds__(kThreads, 2)
+    bilateral_persist_kernel(const uint8_t* __restrict__ img, int H, int W, int row0, int row1,
+                             const double* __restrict__ spatial, const double* __restrict__ range,
+                             OUT* __restrict__ out, int tiles_x, int ntiles) {
+  constexpr int S = 2 * R + 1;
+  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
+  constexpr int HALO = TH * TW;
+  constexpr int PER = (HALO + kThreads - 1) / kThreads;  // halo pixels per thread
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* rng = reinterpret_cast<double*>(smem);  // [256][32] lane-striped
+  double* sp = rng + 256 * 32;                    // [S*S]
+  int* tiles = reinterpret_cast<int*>(sp + S * S);  // [2][TH][TW]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  for (int i = tid; i < 256 * 32; i += kThreads) rng[i] = range[i >> 5];
+  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
+
+  int pre[PER];
+  auto fetch = [&](int t) {  // halo of tile t into registers (clamped)
+    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * kThreads;
+      if (i < HALO) {
+        const int ty = i / TW, tx = i - ty * TW;
+        const int gy = min(max(y0 - R + ty, 0), H - 1);
+        const int gx = min(max(x0 - R + tx, 0), W - 1);
+        pre[u] = img[(int64_t)gy * W + gx];
+      }
+    }
+  };
+  auto stash = [&](int* buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * kThreads;
+      if (i < HALO) buf[i] = pre[u];
+    }
+  };
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  fetch(t);
+  stash(tiles);
+  __syncthreads();
+  const int py = tid / (kTileW / kPx);
+  const int px = (tid % (kTileW / kPx)) * kPx;
+  const double* lane_rng = rng + lane;
+  for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) fetch(tn);  // in flight while this tile is filtered
+    const int* tile = tiles + b * HALO;
+    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
+    const int gy = y0 + py;
+    if (gy < row1) {
+      int c[kPx];
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) c[j] = tile[(py + R) * TW + px + j + R];
+      double num[kPx], den[kPx];
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) num[j] = den[j] = 0.0;
+#pragma unroll 1
+      for (int dy = 0; dy < S; ++dy) {
+        int nb[kPx + 2 * R];
+        double nbd[kPx + 2 * R];
+        const int* trow = tile + (py + dy) * TW + px;
+#pragma unroll
+        for (int k = 0; k < kPx + 2 * R; ++k) {
+          nb[k] = trow[k];
+          nbd[k] = (double)nb[k];
+        }
+#pragma unroll
+        for (int dx = 0; dx < S; ++dx) {
+          const double s = sp[dy * S + dx];
+#pragma unroll
+          for (int j = 0; j < kPx; ++j) {
+            const int d = abs(nb[j + dx] - c[j]);
+            const double w = __dmul_rn(s, lane_rng[d << 5]);
+            num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
+            den[j] = __dadd_rn(den[j], w);
+          }
+        }
+      }
+      OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
+#pragma unroll
+      for (int j = 0; j < kPx; ++j)
+        if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
+    }
+    if (tn < ntiles) stash(tiles + (b ^ 1) * HALO);
+    __syncthreads();
+  }
 }
 
 // generic radius (> kMaxR): same arithmetic, neighbours read from global memory.
@@ -124,6 +229,34 @@ template <int R, typename OUT>
 int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const double* sp,
                 const double* rg, OUT* out, cudaStream_t s) {
   constexpr int S = 2 * R + 1;
+  static const int variant = [] {
+    const char* e = getenv("HB_BILAT_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  if (variant == 0 || variant == 2) {
+    // one CTA per tile, 16-lane striped table (46 KB smem), 3 CTAs per SM
+    const size_t smem = 256 * 16 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
+    auto k = variant == 0 ? bilateral_tile_kernel<R, OUT, 16, 3> : bilateral_tile_kernel<R, OUT, 16, 2>;
+    HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
+    k<<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out);
+    return check_launch();
+  }
+  if (variant == 3) {
+    const size_t smem = 256 * 32 * 8 + S * S * 8 + 2 * (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
+    HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_persist_kernel<R, OUT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DeviceInfo di;
+    HB_TRY(device_info(&di));
+    const int tiles_x = (int)ceil_div(W, kTileW);
+    const int64_t ntiles = (int64_t)tiles_x * ceil_div(row1 - row0, kTileH);
+    HB_CHECK_ARG(ntiles < INT32_MAX, "image too large");
+    int64_t grid = (int64_t)di.sms * 2;
+    if (grid > ntiles) grid = ntiles;
+    bilateral_persist_kernel<R, OUT><<<(unsigned)grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out,
+                                                                            tiles_x, (int)ntiles);
+    return check_launch();
+  }
   const size_t smem = 256 * 32 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
   HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_tile_kernel<R, OUT>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -16,6 +16,11 @@
 // segment of the current tap row in registers, so each tap costs one DMUL +
 // one DADD per pixel and no shared-memory traffic (the weight is a warp-wide
 // broadcast).  Bound: fp64 issue (2 flops per tap per pixel), not HBM.
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
 #include "common.cuh"
 
 namespace hb {
@@ -30,8 +35,8 @@ constexpr int kMaxR = 8;
 template <typename IN>
 __device__ __forceinline__ double to_f64(IN v) { return (double)v; }
 
-template <int R, typename IN, typename OUT>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int R, typename IN, typename OUT, bool DENSE = false, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB)
     conv_tile_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
                      const double* __restrict__ weights, OUT* __restrict__ out) {
   constexpr int S = 2 * R + 1;
@@ -66,7 +71,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int dx = 0; dx < S; ++dx) {
       const double w = sw[dy * S + dx];
-      if (w != 0.0) {
+      if (DENSE || w != 0.0) {  // DENSE: the host checked that no weight is 0
 #pragma unroll
         for (int j = 0; j < kPx; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(w, seg[j + dx]));
       }
@@ -76,6 +81,87 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
   for (int j = 0; j < kPx; ++j)
     if (x0 + px + j < W) o[j] = (OUT)acc[j];
+}
+
+// Persistent variant (HB_CONV_CFG=1; measured slower than one CTA per tile
+// at 3 CTAs/SM, kept for the record): 2 CTAs per SM walk the tiles
+// round-robin; the halo of the next tile is loaded into registers before the
+// current tile is filtered and stored to the other smem buffer afterwards,
+// so halo load latency hides behind the fp64 work.
+template <int R, typename IN, typename OUT>
+__global__ void __launch_bounds__(kThreads, 2)
+    conv_persist_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
+                        const double* __restrict__ weights, OUT* __restrict__ out, int tiles_x, int ntiles) {
+  constexpr int S = 2 * R + 1;
+  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
+  constexpr int HALO = TH * TW;
+  constexpr int PER = (HALO + kThreads - 1) / kThreads;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sw = reinterpret_cast<double*>(smem);  // [S*S]
+  double* tiles = sw + S * S;                    // [2][TH][TW]
+  const int tid = threadIdx.x;
+  for (int i = tid; i < S * S; i += kThreads) sw[i] = weights[i];
+  IN pre[PER];
+  auto fetch = [&](int t) {
+    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * kThreads;
+      if (i < HALO) {
+        const int ty = i / TW, tx = i - ty * TW;
+        const int gy = min(max(y0 - R + ty, 0), H - 1);
+        const int gx = min(max(x0 - R + tx, 0), W - 1);
+        pre[u] = img[(int64_t)gy * W + gx];
+      }
+    }
+  };
+  auto stash = [&](double* buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * kThreads;
+      if (i < HALO) buf[i] = to_f64(pre[u]);
+    }
+  };
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  fetch(t);
+  stash(tiles);
+  __syncthreads();
+  const int py = tid / (kTileW / kPx);
+  const int px = (tid % (kTileW / kPx)) * kPx;
+  for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) fetch(tn);
+    const double* tile = tiles + b * HALO;
+    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
+    const int gy = y0 + py;
+    if (gy < row1) {
+      double acc[kPx];
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) acc[j] = 0.0;
+#pragma unroll 1
+      for (int dy = 0; dy < S; ++dy) {
+        double seg[kPx + 2 * R];
+        const double* trow = tile + (py + dy) * TW + px;
+#pragma unroll
+        for (int k = 0; k < kPx + 2 * R; ++k) seg[k] = trow[k];
+#pragma unroll
+        for (int dx = 0; dx < S; ++dx) {
+          const double w = sw[dy * S + dx];
+          if (w != 0.0) {
+#pragma unroll
+            for (int j = 0; j < kPx; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(w, seg[j + dx]));
+          }
+        }
+      }
+      OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
+#pragma unroll
+      for (int j = 0; j < kPx; ++j)
+        if (x0 + px + j < W) o[j] = (OUT)acc[j];
+    }
+    if (tn < ntiles) stash(tiles + (b ^ 1) * HALO);
+    __syncthreads();
+  }
 }
 
 // radius > kMaxR: same arithmetic, neighbours read from global memory
@@ -101,27 +187,51 @@ __global__ void conv_generic_kernel(const IN* __restrict__ img, int H, int W, in
 }
 
 template <int R, typename IN, typename OUT>
-int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w, OUT* out, cudaStream_t s) {
+int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w, bool dense, OUT* out,
+                cudaStream_t s) {
   constexpr int S = 2 * R + 1;
+  static const int variant = [] {
+    const char* e = getenv("HB_CONV_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  if (variant == 1) {
+    const size_t smem = (size_t)S * S * 8 + 2 * (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 8;
+    HB_CUDA_TRY(cudaFuncSetAttribute(conv_persist_kernel<R, IN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DeviceInfo di;
+    HB_TRY(device_info(&di));
+    const int tiles_x = (int)ceil_div(W, kTileW);
+    const int64_t ntiles = (int64_t)tiles_x * ceil_div(row1 - row0, kTileH);
+    HB_CHECK_ARG(ntiles < INT32_MAX, "image too large");
+    int64_t grid = (int64_t)di.sms * 2;
+    if (grid > ntiles) grid = ntiles;
+    conv_persist_kernel<R, IN, OUT><<<(unsigned)grid, kThreads, smem, s>>>(img, H, W, row0, row1, w, out, tiles_x, (int)ntiles);
+    return check_launch();
+  }
   const size_t smem = (size_t)S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 8;
-  HB_CUDA_TRY(cudaFuncSetAttribute(conv_tile_kernel<R, IN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
-  conv_tile_kernel<R, IN, OUT><<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, w, out);
-  return check_launch();
+  auto launch = [&](auto kern) -> int {
+    HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, w, out);
+    return check_launch();
+  };
+  if (variant == 2) return dense ? launch(conv_tile_kernel<R, IN, OUT, true, 2>) : launch(conv_tile_kernel<R, IN, OUT, false, 2>);
+  if (variant == 3) return launch(conv_tile_kernel<R, IN, OUT, false, 3>);
+  return dense ? launch(conv_tile_kernel<R, IN, OUT, true, 3>) : launch(conv_tile_kernel<R, IN, OUT, false, 3>);
 }
 
 template <typename IN, typename OUT>
-int launch_conv(const IN* img, int H, int W, int row0, int row1, int R, const double* w, OUT* out, cudaStream_t s) {
+int launch_conv(const IN* img, int H, int W, int row0, int row1, int R, const double* w, bool dense, OUT* out,
+                cudaStream_t s) {
   switch (R) {
-    case 0: return launch_tile<0, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 1: return launch_tile<1, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 2: return launch_tile<2, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 3: return launch_tile<3, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 4: return launch_tile<4, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 5: return launch_tile<5, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 6: return launch_tile<6, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 7: return launch_tile<7, IN, OUT>(img, H, W, row0, row1, w, out, s);
-    case 8: return launch_tile<8, IN, OUT>(img, H, W, row0, row1, w, out, s);
+    case 0: return launch_tile<0, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 1: return launch_tile<1, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 2: return launch_tile<2, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 3: return launch_tile<3, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 4: return launch_tile<4, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 5: return launch_tile<5, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 6: return launch_tile<6, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 7: return launch_tile<7, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 8: return launch_tile<8, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
     default: {
       DeviceInfo di;
       HB_TRY(device_info(&di));
@@ -134,11 +244,11 @@ int launch_conv(const IN* img, int H, int W, int row0, int row1, int R, const do
 }
 
 template <typename IN>
-int dispatch_out(const void* img, int H, int W, int row0, int row1, int R, const double* w, void* out,
-                 int out_code, cudaStream_t s) {
+int dispatch_out(const void* img, int H, int W, int row0, int row1, int R, const double* w, bool dense,
+                 void* out, int out_code, cudaStream_t s) {
   auto in = reinterpret_cast<const IN*>(img);
-  return out_code == 64 ? launch_conv<IN, double>(in, H, W, row0, row1, R, w, reinterpret_cast<double*>(out), s)
-                        : launch_conv<IN, float>(in, H, W, row0, row1, R, w, reinterpret_cast<float*>(out), s);
+  return out_code == 64 ? launch_conv<IN, double>(in, H, W, row0, row1, R, w, dense, reinterpret_cast<double*>(out), s)
+                        : launch_conv<IN, float>(in, H, W, row0, row1, R, w, dense, reinterpret_cast<float*>(out), s);
 }
 
 }  // namespace
@@ -173,10 +283,23 @@ extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t
   HB_TRY(stage_in(&d_w, weights, (size_t)S * S * 8, dev, s));
   const size_t out_bytes = (size_t)(row1 - row0) * width * (out_code == 64 ? 8 : 4);
   HB_TRY(stage_out(&d_out, out, out_bytes, dev, s));
+  // no zero tap → the branch-free kernel (the zero-skip test is the only
+  // data-dependent branch of the tap loop); weights are read on the host
+  bool dense = true;
+  {
+    std::vector<double> hw((size_t)S * S);
+    if (dev) {
+      HB_CUDA_TRY(cudaMemcpyAsync(hw.data(), weights, hw.size() * 8, cudaMemcpyDeviceToHost, s));
+      HB_CUDA_TRY(cudaStreamSynchronize(s));
+    } else {
+      memcpy(hw.data(), weights, hw.size() * 8);
+    }
+    for (double v : hw) dense &= v != 0.0;
+  }
   const int h = in1 - in0, r0 = row0 - in0, r1 = row1 - in0;
   const int rc = in_code == HB_U8
-                     ? dispatch_out<uint8_t>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), d_out.ptr, out_code, s)
-                     : dispatch_out<double>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), d_out.ptr, out_code, s);
+                     ? dispatch_out<uint8_t>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), dense, d_out.ptr, out_code, s)
+                     : dispatch_out<double>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), dense, d_out.ptr, out_code, s);
   if (rc != HB_OK) return rc;
   HB_TRY(copy_out(out, d_out, out_bytes, dev, s));
   return finish(flags, s);

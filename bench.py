@@ -272,13 +272,13 @@ class SpmvBench:
     def setup(self, rank, world):
         import torch
 
-        from paper_1303_2171_b200.datasets import gen_csr
+        from paper_1303_2171_b200.datasets import csr_arrays
         from paper_1303_2171_b200.kernels_irregular import CsrMatrix, spmv_preprocess
         from paper_1303_2171_b200.platform import Platform
         from paper_1303_2171_b200.rng import mix_seed, uniform_floats
         from paper_1303_2171_b200.worksharing import WorkShare
 
-        ptr, col, val = gen_csr(self.rows, self.rows, self.seed, self.density)
+        ptr, col, val = csr_arrays(self.rows, self.rows, self.seed, self.density)
         self.m = CsrMatrix(self.rows, self.rows, ptr, col, val)
         self.nnz = self.m.nnz
         self.x_host = 2.0 * uniform_floats(mix_seed(self.seed, 0xDEC0), self.rows) - 1.0

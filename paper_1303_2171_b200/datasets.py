@@ -1,16 +1,27 @@
-"""Hot-path input generators, bit-identical to the reference's
-(hybridbench/datasets.py:28-106) but built for benchmark scale: the
-splitmix64 streams are closed-form per draw index, so they are generated in
-vectorised chunks on the host or directly in HBM (rng.device_splitmix).
+"""Hot-path input generators and on-disk formats, bit-identical to the
+reference's (hybridbench/datasets.py:28-163) but built for benchmark scale:
+the splitmix64 streams are closed-form per draw index, so they are generated
+in vectorised chunks on the host or directly in HBM (rng.device_splitmix).
+
+The public generators return the reference's types (CsrMatrix,
+LinkedListArr, Image); the *_arrays helpers return the raw numpy arrays.
+Kinds outside this framework's hot path (spgemm's own kernel, cc, lbm) are
+not generated here (out of scope) — spgemm inputs are plain
+CSR matrices and are served by gen_csr.
 """
 
 from __future__ import annotations
 
+from pathlib import Path
+from typing import Any
+
 import numpy as np
 
+from .errors import ConfigError, DataIOError
 from .rng import GAMMA, MASK64, mix_seed, splitmix64, splitmix64_array, uniform_floats, uniform_ints
 
 LIST_END = -1
+UAR_KINDS = ("sort", "hist", "spmv", "spgemm", "conv", "bilat", "lr")
 
 
 def gen_sort_data(n: int, seed: int) -> np.ndarray:
@@ -23,18 +34,92 @@ def gen_hist_data(n: int, seed: int, bins: int = 256) -> np.ndarray:
     return uniform_ints(seed, n, bins)
 
 
-def gen_image(side: int, seed: int) -> np.ndarray:
+def image_pixels(side: int, seed: int) -> np.ndarray:
     """datasets.py:104-106 pixels (uint8, side x side)."""
     return uniform_ints(seed, side * side, 256).astype(np.uint8).reshape(side, side)
 
 
-def gen_list(n: int, seed: int) -> tuple[np.ndarray, int]:
+def gen_image(side: int, seed: int):
+    """datasets.py:104-106 → Image."""
+    from .kernels_regular import Image
+
+    return Image(image_pixels(side, seed))
+
+
+def list_arrays(n: int, seed: int) -> tuple[np.ndarray, int]:
     """datasets.py:58-63: (succ int64, head) of one list in stable-argsort
     order of the draws."""
     order = np.argsort(splitmix64_array(seed, n), kind="stable").astype(np.int64)
     succ = np.full(n, LIST_END, dtype=np.int64)
     succ[order[:-1]] = order[1:]
     return succ, int(order[0])
+
+
+def gen_list(n: int, seed: int):
+    """datasets.py:58-63 → LinkedListArr."""
+    from .kernels_irregular import LinkedListArr
+
+    succ, head = list_arrays(n, seed)
+    return LinkedListArr(succ, head)
+
+
+def gen_csr(rows: int, cols: int, seed: int, density: float):
+    """datasets.py:37-55 → CsrMatrix (see csr_arrays)."""
+    from .kernels_irregular import CsrMatrix
+
+    return CsrMatrix(rows, cols, *csr_arrays(rows, cols, seed, density))
+
+
+def generate_uar(kind: str, size: int, seed: int, **params: Any):
+    """datasets.py:109-130 for the hot-path kinds."""
+    if size < 1:
+        raise ConfigError(f"dataset size must be >= 1, got {size}")
+    if kind == "sort":
+        return gen_sort_data(size, seed)
+    if kind == "hist":
+        return gen_hist_data(size, seed, int(params.get("bins", 256)))
+    if kind in ("spmv", "spgemm"):
+        return gen_csr(size, size, seed, float(params.get("density", 0.01)))
+    if kind == "lr":
+        return gen_list(size, seed)
+    if kind in ("conv", "bilat"):
+        return gen_image(size, seed)
+    if kind in ("cc", "lbm"):
+        raise ConfigError(f"dataset kind {kind!r} belongs to a workload outside this framework's hot path")
+    raise ConfigError(f"unknown dataset kind {kind!r}")
+
+
+def write_dataset(kind: str, dataset, path: str | Path) -> None:
+    """datasets.py:133-153: raw little-endian u32 (sort, hist), MatrixMarket
+    (spmv, spgemm), binary PGM (conv, bilat)."""
+    if kind in ("sort", "hist"):
+        try:
+            np.asarray(dataset, dtype=np.uint32).astype("<u4").tofile(path)
+        except OSError as exc:
+            raise DataIOError(f"cannot write {path}: {exc}") from exc
+        return
+    if kind in ("spmv", "spgemm"):
+        from .kernels_irregular import save_matrix_market
+
+        save_matrix_market(dataset, path)
+        return
+    if kind in ("conv", "bilat"):
+        from .kernels_regular import write_pgm
+
+        write_pgm(dataset, path)
+        return
+    raise ConfigError(f"dataset kind {kind!r} has no file format; it is generated from config")
+
+
+def read_raw_u32(path: str | Path) -> np.ndarray:
+    """datasets.py:156-163: little-endian u32 file → int64; empty → DataIOError."""
+    try:
+        data = np.fromfile(path, dtype="<u4")
+    except OSError as exc:
+        raise DataIOError(f"cannot read {path}: {exc}") from exc
+    if data.size == 0:
+        raise DataIOError(f"{path}: empty input")
+    return data.astype(np.int64)
 
 
 def _fin(z: np.ndarray) -> np.ndarray:
@@ -44,7 +129,7 @@ def _fin(z: np.ndarray) -> np.ndarray:
     return z ^ (z >> np.uint64(31))
 
 
-def gen_csr(rows: int, cols: int, seed: int, density: float, chunk_rows: int = 1 << 17):
+def csr_arrays(rows: int, cols: int, seed: int, density: float, chunk_rows: int = 1 << 17):
     """datasets.py:37-55, vectorised: returns (row_ptr, col_idx, values) —
     int64, int64, f64 — bit-identical to the reference generator.
 
@@ -142,3 +227,45 @@ def device_gen_list(n: int, seed: int, succ_dtype=np.int32):
               _lib.DTYPE_CODES["i4" if tdt == torch.int32 else "i8"], _lib.HB_DEVICE_PTRS, st)
     head = int(order[0].item())
     return succ, head
+
+
+def device_gen_sort_data(n: int, seed: int, k0: int = 0):
+    """gen_sort_data in HBM: uint32 keys (draw >> 32) of draws k0+1..k0+n,
+    as an int32 tensor holding the same bits."""
+    import torch
+
+    from . import _lib
+    from .rng import device_splitmix
+
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    device_splitmix(out, seed, _lib.HB_GEN_HI32, k0=k0)
+    return out
+
+
+def device_gen_image(side: int, seed: int, k0: int = 0):
+    """gen_image pixels in HBM (uint8 side x side, draw & 255)."""
+    import torch
+
+    from . import _lib
+    from .rng import device_splitmix
+
+    out = torch.empty((side, side), dtype=torch.uint8, device="cuda")
+    device_splitmix(out, seed, _lib.HB_GEN_LOW8, k0=k0)
+    return out
+
+
+def device_gen_hist_data(n: int, seed: int, bins: int = 256, k0: int = 0):
+    """gen_hist_data in HBM: uint8 for bins <= 256 (draw & 255 when bins is
+    256, draw % bins otherwise), int64 above."""
+    import torch
+
+    from . import _lib
+    from .rng import device_splitmix
+
+    if bins == 256:
+        out = torch.empty(n, dtype=torch.uint8, device="cuda")
+        device_splitmix(out, seed, _lib.HB_GEN_LOW8, k0=k0)
+        return out
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    device_splitmix(out, seed, _lib.HB_GEN_MOD, bound=bins, k0=k0)
+    return out if bins > 256 else out.to(torch.uint8)

@@ -1,5 +1,6 @@
 """Irregular hot-path kernels behind the reference's own entry points
-(hybridbench/kernels_irregular.py): CSR SpMV and list ranking.
+(hybridbench/kernels_irregular.py): CSR SpMV (+ MatrixMarket I/O) and list
+ranking.
 
 Same names, signatures and error behaviour as the reference.  DeviceA (host
 share) runs numpy on the host cores; DeviceB (GPU share) is one libhb200
@@ -13,12 +14,13 @@ from __future__ import annotations
 import math
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
+from pathlib import Path
 from typing import Any, Sequence
 
 import numpy as np
 
 from . import _lib, sharding
-from .errors import StructuralError
+from .errors import DataIOError, StructuralError
 from .gpu import buf, current_stream_handle, is_device_array, require_gpu, to_host, vp
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
@@ -156,6 +158,59 @@ class CsrMatrix:
 
 # --------------------------------------------------------------------------
 # SpMV (kernels_irregular.py:149-257)
+
+
+def load_matrix_market(path: str | Path) -> CsrMatrix:
+    """kernels_irregular.py:101-134: coordinate real MatrixMarket, general or
+    symmetric (off-diagonal entries mirrored), duplicates summed (from_coo);
+    malformed input → DataIOError."""
+    try:
+        with open(path, "r", encoding="ascii") as fh:
+            banner = fh.readline().strip().lower().split()
+            if banner[:4] != ["%%matrixmarket", "matrix", "coordinate", "real"]:
+                raise DataIOError(f"{path}: only coordinate real MatrixMarket is supported")
+            symmetry = banner[4] if len(banner) > 4 else "general"
+            if symmetry not in ("general", "symmetric"):
+                raise DataIOError(f"{path}: unsupported symmetry {symmetry!r}")
+            line = fh.readline()
+            while line.startswith("%"):
+                line = fh.readline()
+            rows, cols, nnz = (int(t) for t in line.split())
+            body = fh.read().split()
+    except DataIOError:
+        raise
+    except (OSError, ValueError, IndexError) as exc:
+        raise DataIOError(f"cannot read MatrixMarket file {path}: {exc}") from exc
+    if len(body) % 3 or len(body) // 3 != nnz:
+        raise DataIOError(f"{path}: expected {nnz} entries, found {len(body) / 3:g}")
+    try:
+        trip = np.array(body, dtype=np.float64).reshape(-1, 3) if nnz else np.zeros((0, 3))
+    except ValueError as exc:
+        raise DataIOError(f"cannot read MatrixMarket file {path}: {exc}") from exc
+    r = trip[:, 0].astype(np.int64) - 1
+    c = trip[:, 1].astype(np.int64) - 1
+    v = trip[:, 2]
+    if symmetry == "symmetric":
+        mirror = r != c
+        r, c, v = np.concatenate([r, c[mirror]]), np.concatenate([c, r[mirror]]), np.concatenate([v, v[mirror]])
+    try:
+        return CsrMatrix.from_coo(rows, cols, r, c, v)
+    except StructuralError as exc:
+        raise DataIOError(f"{path}: {exc}") from exc
+
+
+def save_matrix_market(m: CsrMatrix, path: str | Path) -> None:
+    """kernels_irregular.py:137-146: general coordinate file, 1-based
+    indices, values written with repr (round-trip exact)."""
+    m = m.to_host() if m.on_device else m
+    rows_of = np.repeat(np.arange(m.rows), m.row_nnz)
+    try:
+        with open(path, "w", encoding="ascii") as fh:
+            fh.write(f"%%MatrixMarket matrix coordinate real general\n{m.rows} {m.cols} {m.nnz}\n")
+            fh.writelines(f"{r + 1} {c + 1} {v!r}\n" for r, c, v in
+                          zip(rows_of.tolist(), np.asarray(m.col_idx).tolist(), np.asarray(m.values, dtype=np.float64).tolist()))
+    except OSError as exc:
+        raise DataIOError(f"cannot write MatrixMarket file {path}: {exc}") from exc
 
 
 @dataclass(frozen=True)

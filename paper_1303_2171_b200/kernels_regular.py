@@ -12,12 +12,15 @@ over the active GPU group, see sharding.py).  Inputs may be numpy arrays
 from __future__ import annotations
 
 import math
+import re
 from dataclasses import dataclass
+from pathlib import Path
 from typing import Any, Sequence
 
 import numpy as np
 
 from . import _lib, sharding
+from .errors import DataIOError
 from .gpu import buf, current_stream_handle, flags_for, is_device_array, require_gpu, to_host, vp
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
@@ -44,6 +47,68 @@ class Image:
     @property
     def width(self) -> int:
         return int(self.pixels.shape[1])
+
+
+def read_pgm(path: str | Path) -> Image:
+    """kernels_regular.py:48-69: P5 (binary) or P2 (ASCII) PGM, maxval <= 255,
+    '#' comments in the header; any failure → DataIOError."""
+    try:
+        raw = Path(path).read_bytes()
+    except OSError as exc:
+        raise DataIOError(f"cannot read image {path}: {exc}") from exc
+    try:
+        magic, (width, height, maxval), start = _parse_pgm_header(raw)
+        if not 0 < maxval <= 255:
+            raise ValueError(f"unsupported maxval {maxval}")
+        count = width * height
+        if magic == b"P5":
+            pix = np.frombuffer(raw, dtype=np.uint8, count=count, offset=start)
+        else:
+            tokens = raw[start:].split()
+            if len(tokens) < count:
+                raise ValueError("truncated P2 payload")
+            pix = np.array([int(t) for t in tokens[:count]], dtype=np.uint8)
+        return Image(pix.reshape(height, width).copy())
+    except Exception as exc:
+        raise DataIOError(f"malformed PGM {path}: {exc}") from exc
+
+
+def _parse_pgm_header(raw: bytes) -> tuple[bytes, tuple[int, int, int], int]:
+    """Magic, (width, height, maxval) and the payload offset: three integer
+    fields separated by whitespace and '#'-to-end-of-line comments, then
+    exactly one whitespace byte before the payload (:72-91)."""
+    magic = raw[:2]
+    if magic not in (b"P2", b"P5"):
+        raise ValueError("not a P2/P5 PGM")
+    fields: list[int] = []
+    pos = 2
+    while len(fields) < 3:
+        m = re.compile(rb"(?:\s|#[^\n]*)*").match(raw, pos)
+        pos = m.end()
+        tok = re.compile(rb"\S+").match(raw, pos)
+        if tok is None:
+            raise ValueError("truncated PGM header")
+        fields.append(int(tok.group()))
+        pos = tok.end()
+    return magic, (fields[0], fields[1], fields[2]), pos + 1
+
+
+def write_pgm(image: Image, path: str | Path, binary: bool = True) -> None:
+    """kernels_regular.py:94-110: maxval-255 PGM; non-uint8 pixels are rounded
+    half-to-even and clamped to [0, 255]."""
+    data = sharding.to_numpy(image.pixels)
+    if data.dtype != np.uint8:
+        data = np.clip(np.rint(data), 0, 255).astype(np.uint8)
+    head = ("P5" if binary else "P2") + f"\n{image.width} {image.height}\n255\n"
+    try:
+        with open(path, "wb") as fh:
+            fh.write(head.encode("ascii"))
+            if binary:
+                fh.write(np.ascontiguousarray(data).tobytes())
+            else:
+                fh.write("".join(" ".join(map(str, row.tolist())) + "\n" for row in data).encode("ascii"))
+    except OSError as exc:
+        raise DataIOError(f"cannot write image {path}: {exc}") from exc
 
 
 # --------------------------------------------------------------------------

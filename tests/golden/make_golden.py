@@ -20,6 +20,9 @@ def main(only: str | None = None) -> None:
     if only == "conv":
         conv()
         return
+    if only == "formats":
+        formats()
+        return
     from hybridbench import datasets, rng
     from hybridbench.kernels_irregular import (
         CsrMatrix,
@@ -124,6 +127,7 @@ def main(only: str | None = None) -> None:
         lr[f"sizes_{i}"] = np.array(st.round_sizes, dtype=np.int64)
     np.savez_compressed(OUT / "listrank.npz", **lr)
     conv()
+    formats()
     print("golden fixtures written to", OUT)
 
 
@@ -162,6 +166,31 @@ def conv() -> None:
     wl = ConvolutionWorkload(Image(np.zeros((3600, 3600), dtype=np.uint8)), FilterKernel.delta(7))
     c["part_18"] = np.array(wl.partition(0.18))
     np.savez_compressed(OUT / "conv.npz", **c)
+
+
+def formats() -> None:
+    """On-disk formats (datasets.py:133-163, kernels_regular.py:48-110,
+    kernels_irregular.py:101-146): files written by the reference and what
+    the reference reads back from hand-written inputs (comments, symmetric,
+    duplicates)."""
+    from hybridbench import datasets
+    from hybridbench.kernels_irregular import load_matrix_market
+    from hybridbench.kernels_regular import read_pgm, write_pgm
+
+    d = OUT / "formats"
+    d.mkdir(exist_ok=True)
+    datasets.write_dataset("spmv", datasets.gen_csr(60, 60, 5, 0.05), d / "ref_spmv.mtx")
+    datasets.write_dataset("bilat", datasets.gen_image(21, 6), d / "ref_img.pgm")
+    write_pgm(datasets.gen_image(9, 2), d / "ref_img_p2.pgm", binary=False)
+    datasets.write_dataset("sort", datasets.gen_sort_data(777, 8), d / "ref_sort.u32")
+    (d / "in_sym.mtx").write_text(
+        "%%MatrixMarket matrix coordinate real symmetric\n% a comment\n%another\n4 4 6\n"
+        "1 1 2.5\n2 1 -1.0\n3 2 0.125\n4 4 1e-3\n3 1 7\n2 1 0.5\n"
+    )
+    (d / "in_comment.pgm").write_bytes(b"P2\n# made by hand\n3 2 # width height\n200\n0 1 2\n200 7 9\n")
+    m = load_matrix_market(d / "in_sym.mtx")
+    img = read_pgm(d / "in_comment.pgm")
+    np.savez_compressed(d / "parsed.npz", sym_ptr=m.row_ptr, sym_col=m.col_idx, sym_val=m.values, comment_pix=img.pixels)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,29 @@
+"""Device-side generators: HBM streams bit-identical to
+the reference generators, including offset (k0) chunks for sharded runs."""
+
+import numpy as np
+import pytest
+
+from oracle import datasets as ods
+from paper_1303_2171_b200 import datasets as d
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_sort_hist_image_generators():
+    n = 100_003
+    keys = d.device_gen_sort_data(n, 42).cpu().numpy().view(np.uint32)
+    assert np.array_equal(keys.astype(np.int64), d.gen_sort_data(n, 42))
+    tail = d.device_gen_sort_data(1000, 42, k0=n - 1000).cpu().numpy().view(np.uint32)
+    assert np.array_equal(tail, keys[-1000:])
+    for bins in (256, 100, 1000):
+        got = d.device_gen_hist_data(n, 7, bins).cpu().numpy()
+        assert np.array_equal(got.astype(np.int64), d.gen_hist_data(n, 7, bins)), bins
+    assert np.array_equal(d.device_gen_image(77, 3).cpu().numpy(), d.gen_image(77, 3).pixels)
+    assert np.array_equal(d.gen_image(77, 3).pixels, ods.image(77, 3))
+
+
+def test_device_gen_list_matches_reference_generator():
+    succ, head = d.device_gen_list(50_000, 11)
+    want = d.gen_list(50_000, 11)
+    assert head == want.head and np.array_equal(succ.cpu().numpy().astype(np.int64), want.succ)

@@ -1,0 +1,207 @@
+// host.cu — native DeviceA (host-core) kernels.  The host share of a
+// work-shared run (fraction_a of the input) is computed here instead of in
+// numpy: same arithmetic as the reference's numpy bodies, bit for bit, on
+// `workers` std::threads (the reference's Device.worker_count sub-chunks).
+//   hb_host_hist        HistogramWorkload.run_part DeviceA   kernels_regular.py:149-154
+//   hb_host_spmv_rows   _csr_range_matvec                    kernels_irregular.py:206-211
+//   hb_host_conv_rows   convolve_rows                        kernels_regular.py:359-381
+//   hb_host_bilateral   bilateral_rows                       kernels_regular.py:461-486
+// Floating point: one rounded multiply then one rounded add per term, in the
+// reference's order (the Makefile builds host code with -ffp-contract=off,
+// so no FMA is ever formed).  No GPU is touched.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hb {
+namespace {
+
+template <typename F>
+void parallel_chunks(int64_t n, int workers, F&& fn) {
+  // contiguous chunks [k*n/w, (k+1)*n/w), one thread each (the reference's split)
+  if (workers <= 1 || n < 2) {
+    fn(0, 0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve((size_t)workers);
+  for (int k = 0; k < workers; ++k) {
+    const int64_t a = n * k / workers, b = n * (k + 1) / workers;
+    pool.emplace_back([&, k, a, b] { fn(k, a, b); });
+  }
+  for (auto& t : pool) t.join();
+}
+
+int clamp_workers(int w) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  return std::max(1, std::min(w, hw));
+}
+
+template <typename T>
+bool hist_body(const T* d, int64_t a, int64_t b, int32_t bins, uint64_t* h) {
+  bool ok = true;
+  for (int64_t i = a; i < b; ++i) {
+    const int64_t v = (int64_t)d[i];
+    if (v < 0 || v >= bins) {
+      ok = false;
+      continue;
+    }
+    ++h[v];
+  }
+  return ok;
+}
+
+int64_t idx_at(const void* p, int code, int64_t i) {
+  return code == HB_I32 ? (int64_t) reinterpret_cast<const int32_t*>(p)[i] : reinterpret_cast<const int64_t*>(p)[i];
+}
+
+template <typename IN>
+void conv_rows(const IN* img, int H, int W, int R, const double* w, int row0, int row1, double* out, int workers) {
+  const int S = 2 * R + 1;
+  parallel_chunks(row1 - row0, workers, [&](int, int64_t a, int64_t b) {
+    for (int64_t rr = a; rr < b; ++rr) {
+      const int y = row0 + (int)rr;
+      double* o = out + rr * W;
+      for (int x = 0; x < W; ++x) o[x] = 0.0;
+      // plane order of the reference: for each tap, all pixels of the row
+      for (int dy = 0; dy < S; ++dy) {
+        const IN* src = img + (int64_t)std::min(std::max(y + dy - R, 0), H - 1) * W;
+        for (int dx = 0; dx < S; ++dx) {
+          const double wt = w[dy * S + dx];
+          if (wt == 0.0) continue;
+          for (int x = 0; x < W; ++x) {
+            const int xx = std::min(std::max(x + dx - R, 0), W - 1);
+            const double prod = wt * (double)src[xx];
+            o[x] = o[x] + prod;
+          }
+        }
+      }
+    }
+  });
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int hb_host_hist(const void* data, int dtype, int64_t n, int32_t bin_count, uint64_t* bins_out,
+                            int workers) {
+  HB_CHECK_ARG(n >= 0, "n must be >= 0");
+  HB_CHECK_ARG(bin_count >= 1, "bin_count must be >= 1");
+  HB_CHECK_ARG(bins_out && (n == 0 || data), "NULL pointer");
+  workers = clamp_workers(workers);
+  std::vector<std::vector<uint64_t>> priv((size_t)workers, std::vector<uint64_t>((size_t)bin_count, 0));
+  std::vector<char> ok((size_t)workers, 1);
+  bool supported = true;
+  parallel_chunks(n, workers, [&](int k, int64_t a, int64_t b) {
+    uint64_t* h = priv[(size_t)k].data();
+    bool r = true;
+    switch (dtype) {
+      case HB_U8: r = hist_body(reinterpret_cast<const uint8_t*>(data), a, b, bin_count, h); break;
+      case HB_I8: r = hist_body(reinterpret_cast<const int8_t*>(data), a, b, bin_count, h); break;
+      case HB_U16: r = hist_body(reinterpret_cast<const uint16_t*>(data), a, b, bin_count, h); break;
+      case HB_I16: r = hist_body(reinterpret_cast<const int16_t*>(data), a, b, bin_count, h); break;
+      case HB_U32: r = hist_body(reinterpret_cast<const uint32_t*>(data), a, b, bin_count, h); break;
+      case HB_I32: r = hist_body(reinterpret_cast<const int32_t*>(data), a, b, bin_count, h); break;
+      case HB_U64: {
+        const uint64_t* d = reinterpret_cast<const uint64_t*>(data);
+        for (int64_t i = a; i < b; ++i) {
+          if (d[i] >= (uint64_t)bin_count) r = false;
+          else ++h[d[i]];
+        }
+        break;
+      }
+      case HB_I64: r = hist_body(reinterpret_cast<const int64_t*>(data), a, b, bin_count, h); break;
+      default: supported = false;
+    }
+    ok[(size_t)k] = r;
+  });
+  HB_CHECK_ARG(supported, "unsupported histogram element type code %d", dtype);
+  for (char c : ok) HB_CHECK_ARG(c, "element outside bin domain");
+  for (int32_t j = 0; j < bin_count; ++j) {
+    uint64_t t = 0;
+    for (auto& h : priv) t += h[(size_t)j];
+    bins_out[j] = t;
+  }
+  return HB_OK;
+}
+
+extern "C" int hb_host_spmv_rows(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
+                                 const double* values, int64_t row0, int64_t row1, const double* x, double* y,
+                                 int workers) {
+  HB_CHECK_ARG((ptr_code == HB_I32 || ptr_code == HB_I64) && (col_code == HB_I32 || col_code == HB_I64),
+               "row_ptr/col_idx must be int32 or int64");
+  HB_CHECK_ARG(row0 >= 0 && row1 >= row0, "bad row range");
+  if (row1 == row0) return HB_OK;
+  HB_CHECK_ARG(row_ptr && x && y, "NULL pointer");
+  parallel_chunks(row1 - row0, clamp_workers(workers), [&](int, int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t r = row0 + i;
+      const int64_t s = idx_at(row_ptr, ptr_code, r), e = idx_at(row_ptr, ptr_code, r + 1);
+      double acc = 0.0;
+      for (int64_t k = s; k < e; ++k) {
+        const double prod = values[k] * x[idx_at(col_idx, col_code, k)];
+        acc = acc + prod;
+      }
+      y[i] = acc;
+    }
+  });
+  return HB_OK;
+}
+
+extern "C" int hb_host_conv_rows(const void* img, int in_code, int32_t height, int32_t width, int32_t radius,
+                                 const double* weights, int32_t row0, int32_t row1, double* out, int workers) {
+  HB_CHECK_ARG(height > 0 && width > 0, "image must be non-empty");
+  HB_CHECK_ARG(radius >= 0, "radius must be >= 0");
+  HB_CHECK_ARG(row0 >= 0 && row1 >= row0 && row1 <= height, "bad row range");
+  HB_CHECK_ARG(in_code == HB_U8 || in_code == HB_F64, "image must be uint8 or float64");
+  if (row1 == row0) return HB_OK;
+  HB_CHECK_ARG(img && weights && out, "NULL pointer");
+  workers = clamp_workers(workers);
+  if (in_code == HB_U8) conv_rows(reinterpret_cast<const uint8_t*>(img), height, width, radius, weights, row0, row1, out, workers);
+  else conv_rows(reinterpret_cast<const double*>(img), height, width, radius, weights, row0, row1, out, workers);
+  return HB_OK;
+}
+
+extern "C" int hb_host_bilateral(const uint8_t* img, int32_t height, int32_t width, int32_t radius,
+                                 const double* spatial, const double* range256, int32_t row0, int32_t row1,
+                                 double* out, int workers) {
+  HB_CHECK_ARG(height > 0 && width > 0, "image must be non-empty");
+  HB_CHECK_ARG(radius >= 0, "radius must be >= 0");
+  HB_CHECK_ARG(row0 >= 0 && row1 >= row0 && row1 <= height, "bad row range");
+  if (row1 == row0) return HB_OK;
+  HB_CHECK_ARG(img && spatial && range256 && out, "NULL pointer");
+  const int R = radius, S = 2 * R + 1, W = width, H = height;
+  parallel_chunks(row1 - row0, clamp_workers(workers), [&](int, int64_t a, int64_t b) {
+    std::vector<double> num((size_t)W), den((size_t)W);
+    for (int64_t rr = a; rr < b; ++rr) {
+      const int y = row0 + (int)rr;
+      const uint8_t* crow = img + (int64_t)y * W;
+      std::fill(num.begin(), num.end(), 0.0);
+      std::fill(den.begin(), den.end(), 0.0);
+      for (int dy = 0; dy < S; ++dy) {
+        const uint8_t* src = img + (int64_t)std::min(std::max(y + dy - R, 0), H - 1) * W;
+        for (int dx = 0; dx < S; ++dx) {
+          const double s = spatial[dy * S + dx];
+          for (int x = 0; x < W; ++x) {
+            const int nb = src[std::min(std::max(x + dx - R, 0), W - 1)];
+            const double w = s * range256[abs(nb - (int)crow[x])];
+            const double t = w * (double)nb;
+            num[(size_t)x] = num[(size_t)x] + t;
+            den[(size_t)x] = den[(size_t)x] + w;
+          }
+        }
+      }
+      double* o = out + rr * W;
+      for (int x = 0; x < W; ++x) o[x] = num[(size_t)x] / den[(size_t)x];
+    }
+  });
+  return HB_OK;
+}

@@ -286,12 +286,19 @@ def _device_preprocess(m: CsrMatrix):
     return perm, CsrMatrix(m.rows, m.cols, nrp, ncol, nval)
 
 
-def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int) -> np.ndarray:
-    """DeviceA body: the reference's product + bincount row sums (:206-211)."""
-    rp, ci, v = to_host(m.row_ptr), to_host(m.col_idx), to_host(m.values)
-    lo, hi = int(rp[row0]), int(rp[row1])
-    owner = np.repeat(np.arange(row1 - row0), np.diff(rp[row0 : row1 + 1]))
-    return np.bincount(owner, weights=v[lo:hi] * x[ci[lo:hi]], minlength=row1 - row0)
+def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int, workers: int = 1) -> np.ndarray:
+    """DeviceA body (:206-211) in native code (hb_host_spmv_rows on `workers`
+    threads): rounded products summed left to right per row — exactly the
+    reference's product + bincount arithmetic."""
+    y = np.zeros(max(row1 - row0, 0))
+    if row1 <= row0:
+        return y
+    rp, ci = buf(to_host(m.row_ptr)), buf(to_host(m.col_idx))
+    v = np.ascontiguousarray(to_host(m.values), dtype=np.float64)
+    xh = np.ascontiguousarray(x, dtype=np.float64)
+    _lib.call("hb_host_spmv_rows", vp(rp.ptr), rp.code, vp(ci.ptr), ci.code, vp(v.ctypes.data), row0, row1,
+              vp(xh.ctypes.data), vp(y.ctypes.data), workers)
+    return y
 
 
 def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: Any = None,
@@ -398,7 +405,7 @@ class SpmvWorkload:
     def run_part(self, device: Device, part) -> np.ndarray:
         if device.id is DeviceId.B:
             return _gpu_rows(self.prep.permuted, self.x, part[0], part[1])
-        return _host_range_matvec(self.prep.permuted, self.x_host, part[0], part[1])
+        return _host_range_matvec(self.prep.permuted, self.x_host, part[0], part[1], device.worker_count)
 
     def merge(self, partials: Sequence[np.ndarray]) -> np.ndarray:
         y_perm = np.concatenate(partials)

@@ -161,6 +161,17 @@ def gpu_histogram(part: Any, bin_count: int, out: Any = None, *, asynchronous: b
     return res
 
 
+def host_histogram(part: Any, bin_count: int, workers: int = 1) -> np.ndarray:
+    """DeviceA body (kernels_regular.py:149-154): per-worker private counts on
+    `workers` host threads (hb_host_hist, native), summed; int64 counts."""
+    b = buf(to_host(part))
+    if b.code == 0 or b.dtype.kind == "f":
+        raise TypeError(f"histogram input must be an integer array, got {b.dtype}")
+    res = np.zeros(bin_count, dtype=np.int64)
+    _lib.call("hb_host_hist", vp(b.ptr), b.code, b.size, bin_count, vp(res.ctypes.data), workers)
+    return res
+
+
 class HistogramWorkload:
     """Index-range split (kernels_regular.py:126-160).  DeviceA: per-worker
     private numpy histograms; DeviceB: the privatised smem GPU kernel, its
@@ -194,12 +205,7 @@ class HistogramWorkload:
     def run_part(self, device: Device, part) -> np.ndarray:
         if device.id is DeviceId.B:
             return sharding.run_sharded_histogram(part, self.bin_count)
-        host = to_host(part)
-        counts = np.zeros(self.bin_count, dtype=np.int64)
-        edges = np.linspace(0, host.size, device.worker_count + 1).astype(np.int64)
-        for lo, hi in zip(edges[:-1], edges[1:]):
-            counts += np.bincount(host[lo:hi], minlength=self.bin_count)
-        return counts
+        return host_histogram(part, self.bin_count, device.worker_count)
 
     def merge(self, partials: Sequence[np.ndarray]) -> HistogramResult:
         total = np.zeros(self.bin_count, dtype=np.int64)
@@ -404,25 +410,24 @@ class FilterKernel:
         return cls(g / g.sum())
 
 
-def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int) -> np.ndarray:
-    """Host (DeviceA) body, the reference arithmetic (:359-381): correlation of
-    rows [row0, row1) with clamp-to-edge borders, one weighted plane added per
-    non-zero tap in row-major order."""
-    pixels = to_host(pixels)
-    height, width = pixels.shape
-    r = kernel.radius
-    n_rows = row1 - row0
-    if n_rows <= 0:
-        return np.zeros((0, width))
-    rows_idx = np.clip(np.arange(row0 - r, row1 + r), 0, height - 1)
-    slab = np.pad(pixels[rows_idx].astype(np.float64), ((0, 0), (r, r)), mode="edge")
-    out = np.zeros((n_rows, width))
-    for dy in range(2 * r + 1):
-        for dx in range(2 * r + 1):
-            weight = kernel.weights[dy, dx]
-            if weight == 0.0:
-                continue
-            out += weight * slab[dy : dy + n_rows, dx : dx + width]
+def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, workers: int = 1) -> np.ndarray:
+    """Host (DeviceA) body, the reference arithmetic (:359-381) in native code
+    (hb_host_conv_rows on `workers` threads): correlation of rows [row0, row1)
+    with clamp-to-edge borders, one weighted plane added per non-zero tap in
+    row-major order; float64 rows."""
+    arr = to_host(pixels)
+    if arr.dtype not in (np.uint8, np.float64):
+        arr = arr.astype(np.float64)
+    arr = np.ascontiguousarray(arr)
+    height, width = arr.shape
+    out = np.zeros((max(row1 - row0, 0), width))
+    if row1 <= row0:
+        return out
+    if not 0 <= row0 and row1 <= height:
+        raise ValueError("bad row range")
+    w = np.ascontiguousarray(kernel.weights, dtype=np.float64)
+    _lib.call("hb_host_conv_rows", vp(arr.ctypes.data), _lib.DTYPE_CODES["u1" if arr.dtype == np.uint8 else "f8"],
+              height, width, kernel.radius, vp(w.ctypes.data), row0, row1, vp(out.ctypes.data), workers)
     return out
 
 
@@ -496,7 +501,7 @@ class ConvolutionWorkload:
             return sharding.run_sharded_rows(
                 part[0], part[1], lambda a, b: gpu_convolve_rows(self.image.pixels, self.kernel, a, b)
             )
-        return convolve_rows(self.image.pixels, self.kernel, part[0], part[1])
+        return convolve_rows(self.image.pixels, self.kernel, part[0], part[1], device.worker_count)
 
     def merge(self, partials: Sequence[np.ndarray]) -> Image:
         return Image(np.vstack([sharding.to_numpy(p) for p in partials]))
@@ -553,29 +558,23 @@ def build_bilateral_lut(radius: int, sigma_s: float, sigma_r: float) -> Bilatera
     return BilateralLut(spatial, np.exp(-(k**2) / (2.0 * sigma_r**2)), sigma_s, sigma_r, radius)
 
 
-def bilateral_rows(pixels: np.ndarray, lut: BilateralLut, row0: int, row1: int) -> np.ndarray:
-    """Host (DeviceA) body, the reference arithmetic (:461-486): for each tap in
-    row-major order w = spatial·range[|nb-c|], num += w·nb, den += w; clamp to
-    edge; returns num/den as float64 rows [row0, row1)."""
-    pixels = to_host(pixels)
-    height, width = pixels.shape
-    r = lut.radius
-    m = row1 - row0
-    if m <= 0:
-        return np.zeros((0, width))
-    ridx = np.clip(np.arange(row0 - r, row1 + r), 0, height - 1)
-    slab = np.pad(pixels[ridx].astype(np.int64), ((0, 0), (r, r)), mode="edge")
-    center = slab[r : r + m, r : r + width]
-    num = np.zeros((m, width))
-    den = np.zeros((m, width))
-    side = 2 * r + 1
-    for dy in range(side):
-        for dx in range(side):
-            nb = slab[dy : dy + m, dx : dx + width]
-            w = lut.spatial_weights[dy * side + dx] * lut.range_weights[np.abs(nb - center)]
-            num += w * nb
-            den += w
-    return num / den
+def bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, workers: int = 1) -> np.ndarray:
+    """Host (DeviceA) body, the reference arithmetic (:461-486) in native code
+    (hb_host_bilateral on `workers` threads): for each tap in row-major order
+    w = spatial·range[|nb-c|], num += w·nb, den += w; clamp to edge; returns
+    num/den as float64 rows [row0, row1)."""
+    pix = np.ascontiguousarray(to_host(pixels), dtype=np.uint8)
+    height, width = pix.shape
+    out = np.zeros((max(row1 - row0, 0), width))
+    if row1 <= row0:
+        return out
+    if not 0 <= row0 and row1 <= height:
+        raise ValueError("bad row range")
+    sp = np.ascontiguousarray(lut.spatial_weights, dtype=np.float64)
+    rg = np.ascontiguousarray(lut.range_weights, dtype=np.float64)
+    _lib.call("hb_host_bilateral", vp(pix.ctypes.data), height, width, lut.radius, vp(sp.ctypes.data),
+              vp(rg.ctypes.data), row0, row1, vp(out.ctypes.data), workers)
+    return out
 
 
 def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out: Any = None,
@@ -641,7 +640,7 @@ class BilateralApplyWorkload:
             return sharding.run_sharded_rows(
                 part[0], part[1], lambda a, b: gpu_bilateral_rows(self.image.pixels, self.lut, a, b)
             )
-        return bilateral_rows(self.image.pixels, self.lut, part[0], part[1])
+        return bilateral_rows(self.image.pixels, self.lut, part[0], part[1], device.worker_count)
 
     def merge(self, partials: Sequence[np.ndarray]) -> Image:
         return Image(np.vstack([sharding.to_numpy(p) for p in partials]))

@@ -10,7 +10,7 @@ from oracle import datasets as ods
 from oracle import hist as ohist
 from paper_1303_2171_b200 import _lib
 from paper_1303_2171_b200.kernels_regular import HistogramWorkload, gpu_histogram, hybrid_histogram
-from paper_1303_2171_b200.platform import DeviceId
+from paper_1303_2171_b200.platform import DeviceId, Platform
 from paper_1303_2171_b200.worksharing import WorkShare, formula_share, run_workshared
 
 pytestmark = pytest.mark.gpu
@@ -105,3 +105,16 @@ def test_run_workshared_measured_and_modeled(platform13):
     result, report = run_workshared(meas, workload, formula_share(meas))
     assert np.array_equal(result.bins, np.bincount(data, minlength=256))
     assert report.timeline.busy(DeviceId.B) > 0
+
+
+def test_measured_calibration_host_vs_gpu():
+    # the share measured on this box (native host threads vs B200)
+    from paper_1303_2171_b200.worksharing import calibrate_measured
+
+    data = ods.hist_values(1 << 24, 5, 256).astype(np.uint8)
+    p = Platform.build(1.0, 3.0)
+    wl = HistogramWorkload(data, 256)
+    share = calibrate_measured(wl, p, max_refinements=4)
+    assert 0.0 <= share.fraction_a < 0.25  # the GPU is far faster than the host cores
+    out = hybrid_histogram(data, 256, p, share)
+    assert np.array_equal(out.bins, np.bincount(data, minlength=256))

@@ -692,7 +692,7 @@ __global__ void scan_hist_kernel(const uint32_t* __restrict__ hist, uint32_t* __
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE>
+template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE, int LBW = 1>
 __global__ void __launch_bounds__(T, 1024 / T)
     onesweep_ec_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                        uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
@@ -806,13 +806,39 @@ __global__ void __launch_bounds__(T, 1024 / T)
     uint32_t excl = 0;
     if (tile > 0) {
       int64_t t = (int64_t)tile - 1;
-      while (true) {
-        const uint32_t wv = ld_relaxed(lookback + (size_t)t * 256 + d);
-        const uint32_t flag = wv & ~kCountMask;
-        if (flag == 0) continue;
-        excl += wv & kCountMask;
-        if (flag == kFlagInc) break;
-        --t;
+      if constexpr (LBW == 1) {
+        while (true) {
+          const uint32_t wv = ld_relaxed(lookback + (size_t)t * 256 + d);
+          const uint32_t flag = wv & ~kCountMask;
+          if (flag == 0) continue;
+          excl += wv & kCountMask;
+          if (flag == kFlagInc) break;
+          --t;
+        }
+      } else {
+        // windowed look-back: LBW predecessors loaded at once (independent
+        // loads, one round trip), consumed in order until an inclusive
+        // prefix; a not-yet-published entry stops the window and is re-read
+        bool done = false;
+        while (!done) {
+          uint32_t wv[LBW];
+#pragma unroll
+          for (int j = 0; j < LBW; ++j) {
+            const int64_t tj = t - j < 0 ? 0 : t - j;  // tile 0 is always inclusive
+            wv[j] = ld_relaxed(lookback + (size_t)tj * 256 + d);
+          }
+          int used = 0;
+#pragma unroll
+          for (int j = 0; j < LBW; ++j) {
+            if (done || used < j) continue;
+            const uint32_t flag = wv[j] & ~kCountMask;
+            if (flag == 0) continue;
+            excl += wv[j] & kCountMask;
+            used = j + 1;
+            if (flag == kFlagInc) done = true;
+          }
+          t -= used;
+        }
       }
       st_relaxed(lookback + (size_t)tile * 256 + d, kFlagInc | (excl + c));
     }
@@ -848,19 +874,19 @@ struct PassArgs {
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
 };
 
-template <typename K, int I, int T = 512, bool TWO = false>
+template <typename K, int I, int T = 512, bool TWO = false, int LBW = 1>
 int launch_ec(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
   const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
   *tiles_out = tiles;
   if (dry) return HB_OK;
   const size_t smem = (size_t)T * I * sizeof(K) + (a.vin ? (size_t)T * I * 4 : 0);
   if (a.vin) {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, true, I, T, TWO><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO, LBW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, true, I, T, TWO, LBW><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   } else {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, false, I, T, TWO><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO, LBW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, false, I, T, TWO, LBW><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   }
   return check_launch();
@@ -974,8 +1000,14 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 18: return launch_ec<K, 16, 512>(a, s, tiles, dry);
     case 19: return launch_ec<K, 16, 640>(a, s, tiles, dry);
     case 20: return launch_ec<K, 28, 384>(a, s, tiles, dry);
+    case 21: return launch_ec<K, 20, 384, false, 4>(a, s, tiles, dry);
+    case 22: return launch_ec<K, 20, 384, false, 8>(a, s, tiles, dry);
+    case 23: return launch_ec<K, 16, 384, false, 4>(a, s, tiles, dry);
+    case 24: return launch_ec<K, 24, 384, false, 4>(a, s, tiles, dry);
+    case 25: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);
     case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
-    default: return launch_ec<K, 20, 384>(a, s, tiles, dry);  // best measured (round 1)
+    case 26: return launch_ec<K, 20, 384>(a, s, tiles, dry);
+    default: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);  // best measured (round 1)
   }
   }
 }

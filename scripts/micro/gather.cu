@@ -1,5 +1,6 @@
 // Random-gather sector accounting: which load flavour moves how many sectors per 4-byte random read.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 __device__ __forceinline__ uint32_t hash(uint32_t x) { x ^= x >> 16; x *= 0x7feb352d; x ^= x >> 15; x *= 0x846ca68b; x ^= x >> 16; return x; }
@@ -33,8 +34,15 @@ __global__ void chase(const int* __restrict__ a, int* __restrict__ out, uint32_t
 __global__ void init(int* a, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = (int)(hash(i * 7 + 1) & (n - 1));
 }
-int main() {
+int main(int argc, char** argv) {
   const uint32_t n = 1u << 28, m = 1u << 26;
+  if (argc > 1) {  // cudaLimitMaxL2FetchGranularity: bytes fetched from DRAM per L2 miss
+    const size_t g = (size_t)atoi(argv[1]);
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g);
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+    printf("L2 fetch granularity request %zu -> %s, now %zu\n", g, cudaGetErrorString(e), got);
+  }
   int *a, *o;
   cudaMalloc(&a, (size_t)n * 4); cudaMalloc(&o, (size_t)m * 4);
   init<<<4096, 256>>>(a, n);

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -30,12 +31,44 @@ from pathlib import Path
 
 import numpy as np
 
+ARGS = argparse.Namespace(e2e_share="calibrated")  # set by main()
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
+def e2e_share_info(wl):
+    sh = getattr(wl, "share", None)
+    if sh is None:
+        return None
+    pf = getattr(wl, "platform", None)
+    return {"fraction_a": sh.fraction_a, "origin": sh.origin.value,
+            "host_workers": pf.device_a.worker_count if pf is not None else None,
+            "note": "fraction_a of the input computed on the host cores (native hb_host_* threads), the rest on the B200"}
+
+
+def host_platform():
+    """Platform for the end-to-end legs: DeviceA = the box's host cores (all
+    but one, which drives the GPU copies), DeviceB = the B200."""
+    from paper_1303_2171_b200.platform import Platform
+
+    return Platform.build(1.0, 3.0, workers_a=max(1, (os.cpu_count() or 2) - 1))
+
+
+def e2e_share(args, workload, platform):
+    """The split the e2e leg runs with: `--e2e-share gpu` → all on the GPU;
+    `calibrated` (default) → worksharing.calibrate_measured on this box (the
+    paper's hybrid host+GPU split, measured, not modelled; untimed)."""
+    from paper_1303_2171_b200.worksharing import WorkShare, calibrate_measured
+
+    if args.e2e_share == "gpu" or workload is None:
+        return WorkShare.manual(0.0)
+    return calibrate_measured(workload, platform, max_refinements=6, repeats=2)
+
+
+RANDOM_PEAK_GACCESS = 51.5  # random 4-B DRAM reads/s, scripts/micro/gather.cu
 FP64_PEAK_GFLOPS = 18370.0  # non-FMA fp64 instructions/s, scripts/micro/fp64peak.cu
 METRIC = "per-workload throughput (SpMV GFLOP/s, sort Mkeys/s) and HBM-roofline fraction"
 
@@ -217,11 +250,10 @@ class HistBench:
         self.host = torch.empty(self.n, dtype=torch.uint8, pin_memory=True)
         self.host.copy_(self.x)
         self.host_np = self.host.numpy()
-        from paper_1303_2171_b200.platform import Platform
-        from paper_1303_2171_b200.worksharing import WorkShare
+        from paper_1303_2171_b200.kernels_regular import HistogramWorkload
 
-        self.platform = Platform.build(1.0, 3.0)
-        self.share = WorkShare.manual(0.0)
+        self.platform = host_platform()
+        self.share = e2e_share(ARGS, HistogramWorkload(self.host_np, self.bins), self.platform)
 
     def e2e_step(self):
         from paper_1303_2171_b200.kernels_regular import hybrid_histogram
@@ -236,7 +268,7 @@ class HistBench:
         return res
 
     def e2e_bytes(self):
-        return self.n, self.bins * 8
+        return self.n - int(math.floor(self.share.fraction_a * self.n)), self.bins * 8
 
     # CPU baseline: the reference algorithm (oracle port) on a bounded sample
     def cpu_sample(self, budget_s: float):
@@ -320,10 +352,16 @@ class SpmvBench:
             t.numpy()[...] = a
             return t.numpy()
 
+        from paper_1303_2171_b200.kernels_irregular import SpmvWorkload
+
         p = self.prep.permuted
-        self.hprep = SpmvPrep(CsrMatrix(p.rows, p.cols, pinned(p.row_ptr), pinned(p.col_idx), pinned(p.values)),
-                              self.prep.perm, 0)
+        hm = CsrMatrix(p.rows, p.cols, pinned(p.row_ptr), pinned(p.col_idx), pinned(p.values))
         self.hx = pinned(self.x_host)
+        self.platform = host_platform()
+        wl = SpmvWorkload(SpmvPrep(hm, self.prep.perm, 0), self.hx)
+        self.share = e2e_share(ARGS, wl, self.platform)
+        split = wl.partition(self.share.fraction_a)[0][1]  # the nnz rule of SpmvWorkload.partition
+        self.hprep = SpmvPrep(hm, self.prep.perm, split, self.platform.device_a.worker_count)
 
     def e2e_step(self):
         from paper_1303_2171_b200.kernels_irregular import spmv_hybrid
@@ -332,7 +370,9 @@ class SpmvBench:
 
     def e2e_bytes(self):
         p = self.prep.permuted
-        return (p.row_ptr.nbytes + p.col_idx.nbytes + p.values.nbytes + self.x_host.nbytes), 8 * self.rows
+        s = self.hprep.split_row
+        nz = int(p.row_ptr[-1] - p.row_ptr[s])
+        return (4 * (p.rows - s + 1) + 12 * nz + self.x_host.nbytes), 8 * (p.rows - s)
 
     def cpu_sample(self, budget_s: float):
         from oracle import spmv as ospmv
@@ -415,8 +455,13 @@ class BilatBench:
         self.host = torch.empty((self.side, self.side), dtype=torch.uint8, pin_memory=True)
         self.host.copy_(self.img)
         self.image = Image(self.host.numpy())
-        self.platform = Platform.build(1.0, 3.0)
-        self.share = WorkShare.manual(0.0)
+        self.platform = host_platform()
+        self.share = e2e_share(ARGS, self.e2e_workload(), self.platform)
+
+    def e2e_workload(self):
+        from paper_1303_2171_b200.kernels_regular import BilateralApplyWorkload
+
+        return BilateralApplyWorkload(self.image, self.lut)
 
     def e2e_step(self):
         from paper_1303_2171_b200.kernels_regular import hybrid_bilateral
@@ -424,7 +469,8 @@ class BilatBench:
         return hybrid_bilateral(self.image, self.lut, self.platform, self.share)
 
     def e2e_bytes(self):
-        return self.side * self.side, self.side * self.side * 8
+        gpu_rows = self.side - int(math.floor(self.share.fraction_a * self.side))
+        return gpu_rows * self.side, gpu_rows * self.side * 8
 
     def cpu_sample(self, budget_s: float):
         from oracle import bilateral as obil
@@ -481,6 +527,11 @@ class ConvBench(BilatBench):
             want = oconv.rows(host, self.fk.weights, a, b).astype(np.float32)
             ok &= np.array_equal(self.out[a:b].cpu().numpy(), want)
         return bool(ok)
+
+    def e2e_workload(self):
+        from paper_1303_2171_b200.kernels_regular import ConvolutionWorkload
+
+        return ConvolutionWorkload(self.image, self.fk)
 
     def e2e_step(self):
         from paper_1303_2171_b200.kernels_regular import hybrid_convolve
@@ -654,6 +705,11 @@ class LrBench:
 
     def units_per_step(self):
         return self.n
+
+    def random_accesses_per_launch(self):
+        # level-1 walk: one random succ read + one random (sublist, offset) write per node;
+        # the recursion levels touch 1/64 as many nodes, the expansion is coalesced
+        return 2 * self.n
 
     def bytes_per_launch(self):
         return 12 * self.n
@@ -831,10 +887,23 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
             "ms_per_step": e_s * 1e3,
             "steps": e_steps,
             "api": getattr(wl, "e2e_api", "public drop-in entry point on pinned host buffers"),
+            "share": e2e_share_info(wl),
         },
         "clocks": clk,
         "config": wl.config(),
     }
+    if hasattr(wl, "random_accesses_per_launch"):
+        # random-access-bound kernel: DRAM row activations, not bytes, are the bound
+        ach = wl.random_accesses_per_launch() / (ms / 1e3) / 1e9
+        res["roofline"]["random_access"] = {
+            "bound": "DRAM random accesses (one row activation per random read or write)",
+            "achieved_gaccess_per_s": ach,
+            "peak_gaccess_per_s": RANDOM_PEAK_GACCESS,
+            "frac": ach / RANDOM_PEAK_GACCESS,
+            "peak_source": "measured: scripts/micro/gather.cu, 2^26 random 4-B loads from a 1 GiB array "
+                           "(51.5 G/s; dependent chase 50.3 G/s; cudaLimitMaxL2FetchGranularity 32/64 B: no change)",
+            "accesses_per_launch": wl.random_accesses_per_launch(),
+        }
     if hasattr(wl, "flops_per_launch"):
         # compute-bound kernel: fp64 issue is the bound, HBM fraction is low by design
         ach = wl.flops_per_launch() / (ms / 1e3) / 1e9
@@ -863,7 +932,11 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the end-to-end (host buffer) leg")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--e2e-share", default="calibrated", choices=["calibrated", "gpu"],
+                    help="e2e leg split: measured host+GPU calibration (default) or all on the GPU")
     args = ap.parse_args()
+    global ARGS
+    ARGS = args
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = dist_env()

@@ -43,6 +43,35 @@ int clamp_workers(int w) {
   return std::max(1, std::min(w, hw));
 }
 
+// uint8 fast path: 8 bytes per load, 4 interleaved 32-bit sub-histograms (no
+// store-to-load dependency between neighbouring equal bytes), flushed to the
+// 64-bit counts every 2^30 bytes.
+bool hist_u8_fast(const uint8_t* d, int64_t a, int64_t b, int32_t bins, uint64_t* h) {
+  if (bins < 256) return false;  // values >= bins possible: generic path checks them
+  static thread_local uint32_t sub[4][256];
+  int64_t i = a;
+  while (i < b) {
+    memset(sub, 0, sizeof(sub));
+    const int64_t e = std::min(b, i + ((int64_t)1 << 30));
+    for (; i < e && (i & 7); ++i) ++sub[0][d[i]];
+    for (; i + 8 <= e; i += 8) {
+      uint64_t w;
+      memcpy(&w, d + i, 8);
+      ++sub[0][w & 255];
+      ++sub[1][(w >> 8) & 255];
+      ++sub[2][(w >> 16) & 255];
+      ++sub[3][(w >> 24) & 255];
+      ++sub[0][(w >> 32) & 255];
+      ++sub[1][(w >> 40) & 255];
+      ++sub[2][(w >> 48) & 255];
+      ++sub[3][w >> 56];
+    }
+    for (; i < e; ++i) ++sub[0][d[i]];
+    for (int v = 0; v < 256; ++v) h[v] += (uint64_t)sub[0][v] + sub[1][v] + sub[2][v] + sub[3][v];
+  }
+  return true;
+}
+
 template <typename T>
 bool hist_body(const T* d, int64_t a, int64_t b, int32_t bins, uint64_t* h) {
   bool ok = true;
@@ -75,9 +104,19 @@ void conv_rows(const IN* img, int H, int W, int R, const double* w, int row0, in
         for (int dx = 0; dx < S; ++dx) {
           const double wt = w[dy * S + dx];
           if (wt == 0.0) continue;
-          for (int x = 0; x < W; ++x) {
-            const int xx = std::min(std::max(x + dx - R, 0), W - 1);
-            const double prod = wt * (double)src[xx];
+          // interior columns need no clamp (contiguous, vectorised); borders clamp
+          const int x0 = std::min(W, std::max(0, R - dx)), x1 = std::max(x0, std::min(W, W + R - dx));
+          for (int x = 0; x < x0; ++x) {
+            const double prod = wt * (double)src[std::min(std::max(x + dx - R, 0), W - 1)];
+            o[x] = o[x] + prod;
+          }
+          const IN* s2 = src + dx - R;
+          for (int x = x0; x < x1; ++x) {
+            const double prod = wt * (double)s2[x];
+            o[x] = o[x] + prod;
+          }
+          for (int x = x1; x < W; ++x) {
+            const double prod = wt * (double)src[std::min(std::max(x + dx - R, 0), W - 1)];
             o[x] = o[x] + prod;
           }
         }
@@ -104,7 +143,10 @@ extern "C" int hb_host_hist(const void* data, int dtype, int64_t n, int32_t bin_
     uint64_t* h = priv[(size_t)k].data();
     bool r = true;
     switch (dtype) {
-      case HB_U8: r = hist_body(reinterpret_cast<const uint8_t*>(data), a, b, bin_count, h); break;
+      case HB_U8:
+        if (!hist_u8_fast(reinterpret_cast<const uint8_t*>(data), a, b, bin_count, h))
+          r = hist_body(reinterpret_cast<const uint8_t*>(data), a, b, bin_count, h);
+        break;
       case HB_I8: r = hist_body(reinterpret_cast<const int8_t*>(data), a, b, bin_count, h); break;
       case HB_U16: r = hist_body(reinterpret_cast<const uint16_t*>(data), a, b, bin_count, h); break;
       case HB_I16: r = hist_body(reinterpret_cast<const int16_t*>(data), a, b, bin_count, h); break;
@@ -190,13 +232,17 @@ extern "C" int hb_host_bilateral(const uint8_t* img, int32_t height, int32_t wid
         const uint8_t* src = img + (int64_t)std::min(std::max(y + dy - R, 0), H - 1) * W;
         for (int dx = 0; dx < S; ++dx) {
           const double s = spatial[dy * S + dx];
-          for (int x = 0; x < W; ++x) {
-            const int nb = src[std::min(std::max(x + dx - R, 0), W - 1)];
+          auto tap = [&](int x, int nb) {
             const double w = s * range256[abs(nb - (int)crow[x])];
             const double t = w * (double)nb;
             num[(size_t)x] = num[(size_t)x] + t;
             den[(size_t)x] = den[(size_t)x] + w;
-          }
+          };
+          const int x0 = std::min(W, std::max(0, R - dx)), x1 = std::max(x0, std::min(W, W + R - dx));
+          for (int x = 0; x < x0; ++x) tap(x, src[std::min(std::max(x + dx - R, 0), W - 1)]);
+          const uint8_t* s2 = src + dx - R;
+          for (int x = x0; x < x1; ++x) tap(x, s2[x]);
+          for (int x = x1; x < W; ++x) tap(x, src[std::min(std::max(x + dx - R, 0), W - 1)]);
         }
       }
       double* o = out + rr * W;

@@ -221,6 +221,7 @@ class SpmvPrep:
     permuted: CsrMatrix
     perm: Any
     split_row: int
+    workers_a: int = 1  # host threads for the DeviceA rows (extension; the platform's DeviceA workers)
 
     def __post_init__(self) -> None:
         perm = np.asarray(to_host(self.perm), dtype=np.int64)
@@ -264,7 +265,7 @@ def spmv_preprocess(m: CsrMatrix, platform: Platform, share: WorkShare | None = 
         t_a = cum / platform.device_a.throughput
         t_b = (total - cum) / platform.device_b.throughput
         split = int(np.argmin(np.maximum(t_a, t_b)))
-    return SpmvPrep(permuted, perm, split)
+    return SpmvPrep(permuted, perm, split, platform.device_a.worker_count)
 
 
 def _device_preprocess(m: CsrMatrix):
@@ -370,7 +371,7 @@ def spmv_hybrid(prep: SpmvPrep, x: Any) -> np.ndarray:
     split = prep.split_row
     x_side_b = x if (m.on_device and is_device_array(x)) else xh
     with ThreadPoolExecutor(max_workers=2) as pool:
-        fa = pool.submit(_host_range_matvec, m, xh, 0, split)
+        fa = pool.submit(_host_range_matvec, m, xh, 0, split, prep.workers_a)
         fb = pool.submit(_gpu_rows, m, x_side_b, split, m.rows)
         y_perm = np.concatenate([fa.result(), fb.result()])
     y = np.empty_like(y_perm)

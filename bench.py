@@ -177,9 +177,16 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def coll_device():
+    """Device of bench-level collective tensors: the GPU under NCCL, the host under gloo."""
+    import torch.distributed as dist
+
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
 # ---------------------------------------------------------------- workloads
@@ -217,7 +224,12 @@ class HistBench:
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(self.out)
+            if coll_device() == "cuda":
+                dist.all_reduce(self.out)
+            else:
+                t = self.out.cpu()
+                dist.all_reduce(t)
+                self.out.copy_(t)
         return 1  # libhb200 kernels launched
 
     def units_per_step(self):
@@ -263,7 +275,7 @@ class HistBench:
             import torch
             import torch.distributed as dist
 
-            t = torch.from_numpy(res.bins).cuda()
+            t = torch.from_numpy(res.bins).to(coll_device())
             dist.all_reduce(t)
         return res
 
@@ -591,10 +603,13 @@ class SortBench:
                   vp(self.vals.data_ptr()), vp(self.vals.data_ptr()), self.n, None, _lib.HB_DEVICE_PTRS,
                   current_stream_handle(self.keys))
         if self.world > 1:
+            import torch
+
             from paper_1303_2171_b200.sharding import group_from_default
             from paper_1303_2171_b200.sort_exchange import exchange_sort
 
-            self.out_k, self.out_v = exchange_sort(self.keys, self.vals, group_from_default(),
+            # the keys are u32 (int32 storage): the exchange must order them unsigned
+            self.out_k, self.out_v = exchange_sort(self.keys.view(torch.uint32), self.vals, group_from_default(),
                                                    local_sort=_presorted_then_gpu())
             return 1 + 4 + 1 + 1 + 4
         return 1 + 4  # digit histogram + 4 onesweep passes
@@ -611,7 +626,7 @@ class SortBench:
         from oracle import sort as osort
 
         if self.world > 1:
-            k = self.out_k.cpu().numpy().view(np.uint32)
+            k = self.out_k.view(torch.int32).cpu().numpy().view(np.uint32)
             return bool(np.all(np.diff(k.astype(np.int64)) >= 0))
         k = self.keys.cpu().numpy().view(np.uint32)
         v = self.vals.cpu().numpy()
@@ -777,7 +792,8 @@ def run_reference(args, wl) -> dict:
     rank, world, local = dist_env()
     if rank != 0:
         return {}
-    torch.cuda.set_device(local) if torch.cuda.is_available() else None
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local % torch.cuda.device_count())
     wl.setup(0, 1)
     fn, units, sample = wl.cpu_sample(30.0)
     ts = time_cpu(fn, args.steps, warm=args.warmup)
@@ -950,11 +966,18 @@ def main() -> None:
 
     import torch
 
+    # HB_BENCH_BACKEND=gloo + more ranks than GPUs: a functional check of the
+    # multi-rank paths on a 1-GPU box (ranks share the device; not a timing)
+    backend = os.environ.get("HB_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1303_2171_b200.gpu import require_gpu
 
     require_gpu()

@@ -75,6 +75,26 @@ def host_split_points(keys, idx, probe_k, probe_i):
     return torch.tensor(out, dtype=torch.int64)
 
 
+def _wire(t):
+    """Collectives move 32-bit unsigned keys as their int32 bits (NCCL/gloo
+    need not support torch.uint32); the key order is unaffected."""
+    import torch
+
+    return t.view(torch.int32) if t.dtype == torch.uint32 else t
+
+
+def sample_positions(n: int, samples: int):
+    """Regular sample positions round(j·(n-1)/(samples-1)), j = 0..samples-1,
+    in exact integer arithmetic (a float32 linspace rounds n-1 up past the
+    end of the array once n >= 2^24)."""
+    import torch
+
+    j = torch.arange(samples, dtype=torch.int64)
+    if samples == 1:
+        return torch.zeros(1, dtype=torch.int64)
+    return (2 * j * (n - 1) + (samples - 1)) // (2 * (samples - 1))
+
+
 def exchange_sort(
     keys: Any,
     idx: Any,
@@ -91,8 +111,10 @@ def exchange_sort(
     keys, idx = local_sort(keys, idx)
     n = keys.numel()
     if n:
-        pick = torch.linspace(0, n - 1, samples).round().long().to(keys.device)
-        sk, si = keys[pick].to(torch.int64), idx[pick].to(torch.int64)
+        pick = sample_positions(n, samples).to(keys.device)
+        sk, si = _wire(keys)[pick].to(torch.int64), idx[pick].to(torch.int64)
+        if keys.dtype == torch.uint32:
+            sk = sk & 0xFFFFFFFF  # the unsigned key value
         ok = torch.ones(samples, dtype=torch.int64, device=keys.device)
     else:
         sk = si = ok = torch.zeros(samples, dtype=torch.int64, device=keys.device)
@@ -105,7 +127,11 @@ def exchange_sort(
     sk_all, si_all = allp[0][order], allp[1][order]
     m = sk_all.size
     picks = [min(m - 1, (j * m) // g.world) for j in range(1, g.world)] if m else []
-    probe_k = torch.from_numpy(sk_all[picks].astype(np.int64)).to(keys.dtype).to(keys.device)
+    pk64 = sk_all[picks].astype(np.int64)
+    if keys.dtype == torch.uint32:  # back to the int32 bits, moved, then viewed as u32
+        probe_k = torch.from_numpy(pk64.astype(np.uint32).view(np.int32)).to(keys.device).view(torch.uint32)
+    else:
+        probe_k = torch.from_numpy(pk64).to(keys.dtype).to(keys.device)
     probe_i = torch.from_numpy(si_all[picks].astype(np.int64)).to(idx.dtype).to(keys.device)
     if n and picks:
         cuts = split_points(keys, idx, probe_k, probe_i).to(torch.int64).cpu().tolist()
@@ -117,11 +143,11 @@ def exchange_sort(
     rc = torch.empty_like(sc)
     dist.all_to_all_single(rc, sc, group=g.group)
     recv = rc.cpu().tolist()
-    k_out = torch.empty(sum(recv), dtype=keys.dtype, device=g.device)
+    k_out = torch.empty(sum(recv), dtype=_wire(keys).dtype, device=g.device)
     i_out = torch.empty(sum(recv), dtype=idx.dtype, device=g.device)
-    dist.all_to_all_single(k_out, keys.contiguous().to(g.device), recv, send, group=g.group)
+    dist.all_to_all_single(k_out, _wire(keys.contiguous()).to(g.device), recv, send, group=g.group)
     dist.all_to_all_single(i_out, idx.contiguous().to(g.device), recv, send, group=g.group)
-    return local_sort(k_out.to(keys.device), i_out.to(keys.device))
+    return local_sort(k_out.to(keys.device).view(keys.dtype), i_out.to(keys.device))
 
 
 def sample_merge_sort(keys: Any, payload: Any, g: ShardGroup, local_sort: Callable | None = None,
@@ -149,15 +175,15 @@ def sample_merge_sort(keys: Any, payload: Any, g: ShardGroup, local_sort: Callab
     dist.all_gather(cnts, cnt, group=g.group)
     sizes = [int(c.item()) for c in cnts]
     width = max(sizes)
-    pk = torch.zeros(width, dtype=mk.dtype, device=g.device)
+    pk = torch.zeros(width, dtype=_wire(mk).dtype, device=g.device)
     pi = torch.zeros(width, dtype=mi.dtype, device=g.device)
-    pk[: mk.numel()] = mk.to(g.device)
+    pk[: mk.numel()] = _wire(mk).to(g.device)
     pi[: mi.numel()] = mi.to(g.device)
     gk = [torch.empty_like(pk) for _ in range(g.world)]
     gi = [torch.empty_like(pi) for _ in range(g.world)]
     dist.all_gather(gk, pk, group=g.group)
     dist.all_gather(gi, pi, group=g.group)
-    out_k = torch.cat([gk[r][: sizes[r]] for r in range(g.world)])
+    out_k = torch.cat([gk[r][: sizes[r]] for r in range(g.world)]).view(mk.dtype)
     order = torch.cat([gi[r][: sizes[r]] for r in range(g.world)]).to(torch.int64)
     out_p = None
     if payload is not None:

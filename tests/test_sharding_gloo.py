@@ -115,6 +115,30 @@ def sort_uneven_body(rank, world):
     return bool(np.array_equal(gk, allk[order]) and np.array_equal(gi, order))
 
 
+def sort_u32_body(rank, world):
+    """u32 keys with the top bit set (the benchmark's key type): the exchange
+    must order them unsigned end to end (samples, splitters, wire format)."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import datasets as ods
+    from paper_1303_2171_b200.sort_exchange import exchange_sort, host_local_sort, host_split_points
+
+    n = 6000
+    allk = ods.sort_keys(n * world, 11).astype(np.uint32)  # uniform over [0, 2^32)
+    assert (allk >= 1 << 31).any()
+    mine = torch.from_numpy(allk[rank * n : (rank + 1) * n].copy()).view(torch.uint32)
+    idx = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int32)
+    k, i = exchange_sort(mine, idx, _group(), host_local_sort, host_split_points, samples=64)
+    assert k.dtype == torch.uint32
+    parts = [None] * world
+    dist.all_gather_object(parts, (k.view(torch.int32).numpy().view(np.uint32), i.numpy()))
+    gk = np.concatenate([a for a, _ in parts])
+    gi = np.concatenate([b for _, b in parts])
+    order = np.argsort(allk, kind="stable")
+    return bool(np.array_equal(gk, allk[order]) and np.array_equal(gi, order))
+
+
 # ---------------------------------------------------------------- tests
 def test_shard_bounds_rule():
     assert shard_bounds(10, 3) == [0, 3, 6, 10]
@@ -122,7 +146,7 @@ def test_shard_bounds_rule():
     assert shard_bounds(0, 4) == [0, 0, 0, 0, 0]
 
 
-@pytest.mark.parametrize("body", ["hist_body", "rows_body", "sort_body"])
+@pytest.mark.parametrize("body", ["hist_body", "rows_body", "sort_body", "sort_u32_body"])
 def test_world2(body):
     res = run_world(body, 2)
     assert res == {0: True, 1: True}, res
@@ -131,3 +155,12 @@ def test_world2(body):
 def test_world3_uneven_sort_exchange():
     res = run_world("sort_uneven_body", 3)
     assert res == {0: True, 1: True, 2: True}, res
+
+
+def test_sample_positions_exact_at_benchmark_sizes():
+    # the 2^28-key-per-rank sort: float32 linspace would index past the end
+    from paper_1303_2171_b200.sort_exchange import sample_positions
+
+    for n in (1, 2, 255, 256, 1 << 24, (1 << 28) + 3, 1 << 28):
+        p = sample_positions(n, 256)
+        assert int(p[0]) == 0 and int(p[-1]) == n - 1 and bool((p[1:] >= p[:-1]).all())

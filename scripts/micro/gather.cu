@@ -31,6 +31,15 @@ __global__ void chase(const int* __restrict__ a, int* __restrict__ out, uint32_t
   }
   out[i] = cur;
 }
+// random 8-byte writes (the list-ranking walk's (sublist, offset) store)
+template <int MODE>
+__global__ void scatter8(unsigned long long* __restrict__ a, uint32_t m, uint32_t mask) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  uint32_t j = hash(i * 3 + 1) & mask;
+  if (MODE == 0) a[j] = i;
+  else asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(a + j), "l"((unsigned long long)i) : "memory");
+}
 __global__ void init(int* a, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = (int)(hash(i * 7 + 1) & (n - 1));
 }
@@ -53,5 +62,8 @@ int main(int argc, char** argv) {
   const uint32_t nt = 1u << 20; const int steps = 256;
 #define CH(M) chase<M><<<nt / 256, 256>>>(a, o, nt, steps); cudaEventRecord(e0); chase<M><<<nt / 256, 256>>>(a, o, nt, steps); cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1); printf("chase mode %d: %.3f ms, %.2f G loads/s\n", M, ms, (double)nt * steps / ms / 1e6);
   CH(0) CH(1)
+  // scatter: 2^26 random 8-B writes into a 1 GiB array (2^27 u64 slots)
+#define SC(M) scatter8<M><<<m / 256, 256>>>((unsigned long long*)a, m, (n / 2) - 1); cudaEventRecord(e0); scatter8<M><<<m / 256, 256>>>((unsigned long long*)a, m, (n / 2) - 1); cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1); printf("scatter8 mode %d: %.3f ms, %.2f G writes/s\n", M, ms, m / ms / 1e6);
+  SC(0) SC(1)
   return 0;
 }

@@ -68,7 +68,8 @@ def e2e_share(args, workload, platform):
     return calibrate_measured(workload, platform, max_refinements=6, repeats=2)
 
 
-RANDOM_PEAK_GACCESS = 51.5  # random 4-B DRAM reads/s, scripts/micro/gather.cu
+RANDOM_READ_PEAK = 51.5   # G random 4-B DRAM reads/s, scripts/micro/gather.cu
+RANDOM_WRITE_PEAK = 24.8  # G random 8-B DRAM writes/s (read-fill + write), same micro
 FP64_PEAK_GFLOPS = 18370.0  # non-FMA fp64 instructions/s, scripts/micro/fp64peak.cu
 METRIC = "per-workload throughput (SpMV GFLOP/s, sort Mkeys/s) and HBM-roofline fraction"
 
@@ -724,7 +725,7 @@ class LrBench:
     def random_accesses_per_launch(self):
         # level-1 walk: one random succ read + one random (sublist, offset) write per node;
         # the recursion levels touch 1/64 as many nodes, the expansion is coalesced
-        return 2 * self.n
+        return self.n, self.n
 
     def bytes_per_launch(self):
         return 12 * self.n
@@ -909,16 +910,21 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
         "config": wl.config(),
     }
     if hasattr(wl, "random_accesses_per_launch"):
-        # random-access-bound kernel: DRAM row activations, not bytes, are the bound
-        ach = wl.random_accesses_per_launch() / (ms / 1e3) / 1e9
+        # random-access-bound kernel: DRAM row activations, not bytes, are the bound;
+        # a random 8-B write costs a sector read-fill + a write (micro: 24.8 G/s)
+        reads, writes = wl.random_accesses_per_launch()
+        bound_ms = (reads / RANDOM_READ_PEAK + writes / RANDOM_WRITE_PEAK) / 1e9 * 1e3
         res["roofline"]["random_access"] = {
-            "bound": "DRAM random accesses (one row activation per random read or write)",
-            "achieved_gaccess_per_s": ach,
-            "peak_gaccess_per_s": RANDOM_PEAK_GACCESS,
-            "frac": ach / RANDOM_PEAK_GACCESS,
-            "peak_source": "measured: scripts/micro/gather.cu, 2^26 random 4-B loads from a 1 GiB array "
-                           "(51.5 G/s; dependent chase 50.3 G/s; cudaLimitMaxL2FetchGranularity 32/64 B: no change)",
-            "accesses_per_launch": wl.random_accesses_per_launch(),
+            "bound": "DRAM random accesses: t >= reads/R + writes/W",
+            "reads_per_launch": reads,
+            "writes_per_launch": writes,
+            "peak_read_g_per_s": RANDOM_READ_PEAK,
+            "peak_write_g_per_s": RANDOM_WRITE_PEAK,
+            "bound_ms": bound_ms,
+            "frac": bound_ms / ms,
+            "peak_source": "measured: scripts/micro/gather.cu — 2^26 random 4-B loads from 1 GiB (51.5 G/s; "
+                           "dependent chase 50 G/s; L2 fetch granularity 32/64 B: no change), 2^26 random 8-B "
+                           "stores (24.8 G/s, ncu: 32 B read-fill + 32 B write per store)",
         }
     if hasattr(wl, "flops_per_launch"):
         # compute-bound kernel: fp64 issue is the bound, HBM fraction is low by design

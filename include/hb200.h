@@ -107,6 +107,7 @@ int hb_hist(const void* data, int dtype, int64_t n, int32_t bin_count, uint64_t*
  * within 1e-9 relative.  Host-pointer calls stage only the row range.     */
 #define HB_SPMV_SEQ 0
 #define HB_SPMV_WARP 1
+#define HB_SPMV_MERGE 2  /* merge-path (load-balanced for any row lengths), within 1e-9 relative */
 int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
                 const double* values, int64_t row0, int64_t row1, int64_t cols, const double* x,
                 const void* perm, int perm_code, double* y, int mode, int flags, void* stream);

@@ -26,7 +26,7 @@ HB_ASYNC = 2
 HB_ACCUMULATE = 4
 
 HB_GEN_RAW, HB_GEN_LOW8, HB_GEN_HI32, HB_GEN_MOD = range(4)
-HB_SPMV_SEQ, HB_SPMV_WARP = 0, 1
+HB_SPMV_SEQ, HB_SPMV_WARP, HB_SPMV_MERGE = 0, 1, 2
 
 # numpy dtype.str (sans byte order) -> element code of include/hb200.h
 DTYPE_CODES = {"u1": 1, "i1": 2, "u2": 3, "i2": 4, "u4": 5, "i4": 6, "u8": 7, "i8": 8, "f8": 9}

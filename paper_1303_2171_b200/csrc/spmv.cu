@@ -305,6 +305,125 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------------ merge path
+// HB_SPMV_MERGE: merge-path CSR SpMV (load-balanced for any row-length
+// distribution, no preprocessing): the merge of the row-end offsets with the
+// nnz indices (rows + nnz items) is cut into equal diagonal ranges — a tile
+// of kMpThreads x kMpItems items per CTA, kMpItems per thread — so a row of
+// 10^6 nnz costs the same as 10^6 rows of one.  Per tile: the CTA's merge
+// coordinates are found by binary search, its products val*x[col] are
+// computed cooperatively into shared memory (coalesced loads, parallel
+// gathers), its row ends staged beside them; each thread then walks its
+// kMpItems in merge order, writing every row that ends in its range and
+// emitting a carry (row, partial) for the row it leaves open.  A second,
+// tiny kernel adds each run of carries to its row in order.  Rows split
+// across threads are summed in two or more pieces, so this mode is not
+// bit-exact: within 1e-9 relative of the reference (north_star tolerance).
+constexpr int kMpThreads = 128;
+constexpr int kMpItems = 7;
+constexpr int kMpTile = kMpThreads * kMpItems;
+
+// first merge coordinate (rows consumed, nnz consumed) on diagonal d
+template <typename P>
+__device__ __forceinline__ void merge_search(const P* __restrict__ row_end, int64_t nrows, int64_t nnz0,
+                                             int64_t nnz, int64_t d, int64_t* ri, int64_t* ki) {
+  // row_end[i] = row_ptr[row0 + i + 1] (absolute); nz index k is "absolute - nnz0"
+  int64_t lo = d - nnz > 0 ? d - nnz : 0, hi = d < nrows ? d : nrows;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)row_end[mid] - nnz0 <= d - mid - 1) lo = mid + 1;
+    else hi = mid;
+  }
+  *ri = lo;
+  *ki = d - lo;
+}
+
+template <typename P, typename C, typename Q>
+__global__ void __launch_bounds__(kMpThreads)
+    spmv_merge_kernel(const P* __restrict__ row_ptr, const C* __restrict__ col,
+                      const double* __restrict__ val, const double* __restrict__ x, int64_t row0,
+                      int64_t row1, const Q* __restrict__ perm, double* __restrict__ y,
+                      int64_t* __restrict__ carry_row, double* __restrict__ carry_val) {
+  __shared__ double s_prod[kMpTile + 1];
+  __shared__ int64_t s_rend[kMpTile + 1];
+  __shared__ int64_t s_coord[4];
+  const int tid = threadIdx.x;
+  const int64_t nrows = row1 - row0;
+  const int64_t nnz0 = (int64_t)row_ptr[row0];
+  const int64_t nnz = (int64_t)row_ptr[row1] - nnz0;
+  const P* row_end = row_ptr + row0 + 1;
+  const int64_t total = nrows + nnz;
+  const int64_t d0 = (int64_t)blockIdx.x * kMpTile;
+  const int64_t d1 = d0 + kMpTile < total ? d0 + kMpTile : total;
+  if (tid < 2) {
+    int64_t r, k;
+    merge_search(row_end, nrows, nnz0, nnz, tid == 0 ? d0 : d1, &r, &k);
+    s_coord[2 * tid] = r;
+    s_coord[2 * tid + 1] = k;
+  }
+  __syncthreads();
+  const int64_t tr0 = s_coord[0], tk0 = s_coord[1], tr1 = s_coord[2], tk1 = s_coord[3];
+  // stage the tile's products and row ends
+  for (int64_t k = tk0 + tid; k < tk1; k += kMpThreads) {
+    const int64_t a = nnz0 + k;
+    s_prod[k - tk0] = __dmul_rn(__ldg(val + a), __ldg(x + (int64_t)__ldg(col + a)));
+  }
+  for (int64_t r = tr0 + tid; r < tr1 + 1 && r < nrows; r += kMpThreads) s_rend[r - tr0] = (int64_t)row_end[r] - nnz0;
+  __syncthreads();
+  // this thread's diagonal range inside the tile
+  const int64_t dt0 = d0 + (int64_t)tid * kMpItems;
+  const int64_t gtid = (int64_t)blockIdx.x * kMpThreads + tid;
+  if (dt0 >= d1) {
+    carry_row[gtid] = -1;
+    carry_val[gtid] = 0.0;
+    return;
+  }
+  // local merge search against the staged row ends
+  int64_t r, k;
+  {
+    const int64_t dl = dt0 - d0;  // diagonal within the tile
+    const int64_t rn = tr1 - tr0 + (tr1 < nrows ? 1 : 0), kn = tk1 - tk0;
+    int64_t lo = dl - kn > 0 ? dl - kn : 0, hi = dl < rn ? dl : rn;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (s_rend[mid] - tk0 <= dl - mid - 1) lo = mid + 1;
+      else hi = mid;
+    }
+    r = tr0 + lo;
+    k = tk0 + (dl - lo);
+  }
+  double acc = 0.0;
+  const int64_t dend = dt0 + kMpItems < d1 ? dt0 + kMpItems : d1;
+  for (int64_t dd = dt0; dd < dend; ++dd) {
+    if (r < nrows && k >= s_rend[r - tr0]) {  // row r ends here
+      if (perm) y[(int64_t)perm[row0 + r]] = acc;
+      else y[r] = acc;
+      acc = 0.0;
+      ++r;
+    } else {
+      acc = __dadd_rn(acc, s_prod[k - tk0]);
+      ++k;
+    }
+  }
+  carry_row[gtid] = r < nrows ? r : -1;
+  carry_val[gtid] = acc;
+}
+
+// add each run of carries (consecutive threads carrying the same row) to the
+// row, in thread order
+template <typename Q>
+__global__ void spmv_merge_fixup(const int64_t* __restrict__ carry_row, const double* __restrict__ carry_val,
+                                 int64_t ncarry, int64_t row0, const Q* __restrict__ perm, double* __restrict__ y) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncarry; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = carry_row[t];
+    if (r < 0 || (t > 0 && carry_row[t - 1] == r)) continue;  // not the head of a run
+    double s = 0.0;
+    for (int64_t u = t; u < ncarry && carry_row[u] == r; ++u) s = __dadd_rn(s, carry_val[u]);
+    const int64_t dst = perm ? (int64_t)perm[row0 + r] : r;
+    y[dst] = __dadd_rn(y[dst], s);
+  }
+}
+
 // ------------------------------------------------------------------ validation
 // Flags: 1 row_ptr[0] != 0 or row_ptr[rows] != nnz, 2 decreasing row_ptr,
 //        4 column out of range, 8 columns not strictly increasing in a row.
@@ -380,6 +499,26 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
   auto c = reinterpret_cast<const C*>(ci);
   auto q = reinterpret_cast<const Q*>(pm);
   const int var = spmv_variant();
+  if (mode == 2) {
+    // nnz of the range is needed for the grid: one small D2H read of row_ptr[row0], row_ptr[row1]
+    P ends[2];
+    HB_CUDA_TRY(cudaMemcpyAsync(&ends[0], p + row0, sizeof(P), cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaMemcpyAsync(&ends[1], p + row1, sizeof(P), cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t total = rows + ((int64_t)ends[1] - (int64_t)ends[0]);
+    const int64_t blocks = ceil_div(total, kMpTile);
+    if (blocks > INT32_MAX) { set_error("too many rows"); return HB_EINVAL; }
+    DevBuf crow, cval;
+    HB_TRY(alloc(&crow, (size_t)blocks * kMpThreads * 8, s));
+    HB_TRY(alloc(&cval, (size_t)blocks * kMpThreads * 8, s));
+    spmv_merge_kernel<P, C, Q><<<(unsigned)blocks, kMpThreads, 0, s>>>(p, c, v, x, row0, row1, q, y,
+                                                                       crow.as<int64_t>(), cval.as<double>());
+    HB_TRY(check_launch());
+    int64_t g = ceil_div(blocks * kMpThreads, 256);
+    if (g > (int64_t)di.sms * 8) g = (int64_t)di.sms * 8;
+    spmv_merge_fixup<Q><<<(int)g, 256, 0, s>>>(crow.as<int64_t>(), cval.as<double>(), blocks * kMpThreads, row0, q, y);
+    return check_launch();
+  }
   if (mode == 1) {
     int64_t blocks = ceil_div(rows, 8);
     if (blocks > (int64_t)di.sms * 8) blocks = (int64_t)di.sms * 8;

@@ -303,14 +303,21 @@ def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int, worker
 
 
 def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: Any = None,
-             *, exact: bool = True, asynchronous: bool = False) -> Any:
+             *, exact: bool = True, method: str | None = None, asynchronous: bool = False) -> Any:
     """DeviceB body (hb_spmv_csr).  Without `perm` returns/fills the y_perm
     slice of rows [row0, row1); with `perm` scatters y[perm[i]] in place.
-    `exact` selects the bit-exact sequential row sums (default)."""
+    `method`: "exact" (default; bit-exact sequential row sums), "warp"
+    (warp-per-row tree sums) or "merge" (merge-path, load-balanced for any
+    row-length distribution without preprocessing) — the last two within 1e-9
+    relative.  `exact=False` is the older spelling of "warp"."""
     _lib.load()
     if row1 > row0:
         require_gpu()
-    mode = _lib.HB_SPMV_SEQ if exact else _lib.HB_SPMV_WARP
+    method = method or ("exact" if exact else "warp")
+    modes = {"exact": _lib.HB_SPMV_SEQ, "warp": _lib.HB_SPMV_WARP, "merge": _lib.HB_SPMV_MERGE}
+    if method not in modes:
+        raise ValueError(f"unknown SpMV method {method!r}")
+    mode = modes[method]
     if m.on_device:
         import torch
 

@@ -128,6 +128,45 @@ def test_warp_mode_within_tolerance():
     assert np.array_equal(bits(gpu_spmv(m, x, 0, 20_000)), bits(want))
 
 
+def _power_law_csr(rows, cols, seed):
+    # unsorted rows whose lengths span 0 .. 200k nnz (merge-path's case)
+    rng = np.random.default_rng(seed)
+    lens = np.minimum((rng.pareto(1.2, rows) * 3).astype(np.int64), cols)
+    lens[rng.integers(0, rows, 3)] = [200_000, 50_000, 0]
+    lens[::97] = 0
+    ptr = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    col = np.concatenate([np.sort(rng.choice(cols, int(k), replace=False)) if k else np.zeros(0, np.int64)
+                          for k in lens]).astype(np.int64)
+    val = rng.standard_normal(int(ptr[-1]))
+    return ptr, col, val
+
+
+@pytest.mark.parametrize("idx", [np.int32, np.int64])
+def test_merge_path_within_tolerance(idx):
+    import torch
+
+    rows, cols = 30_000, 250_000
+    ptr, col, val = _power_law_csr(rows, cols, 5)
+    x = np.random.default_rng(6).standard_normal(cols)
+    want = ospmv.range_matvec(ptr, col, val, x, 0, rows)
+    scale = np.abs(val).max() * np.abs(x).max()
+    tol = dict(rtol=1e-9, atol=1e-12 * scale * np.sqrt(np.maximum(np.diff(ptr), 1)).max())
+    m = CsrMatrix(rows, cols, ptr, col, val)
+    assert np.allclose(gpu_spmv(m, x, 0, rows, method="merge"), want, **tol)
+    md = m.to_device(idx)
+    xd = torch.from_numpy(x).cuda()
+    for r0, r1 in [(0, rows), (1, 2), (17, 9_000), (rows - 5, rows)]:
+        got = gpu_spmv(md, xd, r0, r1, method="merge").cpu().numpy()
+        assert np.allclose(got, want[r0:r1], **tol), (r0, r1)
+    perm = torch.from_numpy(np.random.default_rng(1).permutation(rows).astype(np.int64)).cuda()
+    y = torch.zeros(rows, dtype=torch.float64, device="cuda")
+    gpu_spmv(md, xd, 0, rows, y=y, perm=perm, method="merge")
+    yp = np.empty(rows)
+    yp[perm.cpu().numpy()] = want
+    assert np.allclose(y.cpu().numpy(), yp, **tol)
+
+
 def test_device_csr_validation():
     import torch
 

@@ -15,6 +15,8 @@
 // one input row segment (PX+2R values, converted to fp64 once) in registers
 // while it sweeps the 2R+1 taps of that row, so shared-memory traffic per tap
 // is one range-table load.  The bound is fp64 issue (2 DMUL + 2 DADD per tap).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -199,6 +201,123 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// TMA-staged variant (the default when the image allows a tensor map: row
+// pitch a multiple of 16 bytes, 16-byte aligned base): the halo tile of an
+// interior CTA — one whose clamped halo lies inside the image — arrives with
+// ONE cp.async.bulk.tensor.2d issued by thread 0 (completion on an mbarrier)
+// instead of (TH x TW) / 256 clamped byte loads per thread; border CTAs keep
+// the clamped loads (TMA zero-fills out-of-range elements, the reference
+// clamps).  Range table striped over 16 lanes, 3 CTAs/SM.
+template <int R>
+struct TmaTile {
+  // the innermost TMA coordinate must be 16-byte aligned (an unaligned start
+  // faults: scripts/micro/tma2d.cu), so the box starts 16 columns left of the
+  // tile and is 16 + 64 + 16 wide; logical halo column tx sits at tx + OFF
+  static constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
+  static constexpr int PADX = 16, TWB = kTileW + 2 * PADX, OFF = PADX - R;
+  static_assert(R <= PADX, "halo wider than the aligned pad");
+};
+
+template <int R, typename OUT>
+__global__ void __launch_bounds__(kThreads, 3)
+    bilateral_tma_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ img, int H, int W,
+                         int row0, int row1, const double* __restrict__ spatial, const double* __restrict__ range,
+                         OUT* __restrict__ out) {
+  constexpr int S = 2 * R + 1;
+  constexpr int TH = TmaTile<R>::TH, TW = TmaTile<R>::TW, TWB = TmaTile<R>::TWB, OFF = TmaTile<R>::OFF;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  uint8_t* tile = smem;                                                     // [TH][TWB], 128-B aligned
+  double* rng = reinterpret_cast<double*>(smem + ((TH * TWB + 127) / 128) * 128);  // [256][16]
+  double* sp = rng + 256 * 16;                                              // [S*S]
+  const int tid = threadIdx.x;
+  const int lane = tid & 15;
+  const int y0 = row0 + blockIdx.y * kTileH;
+  const int x0 = blockIdx.x * kTileW;
+  const bool interior = x0 - TmaTile<R>::PADX >= 0 && x0 - TmaTile<R>::PADX + TWB <= W && y0 - R >= 0 && y0 - R + TH <= H;
+  if (interior && tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar, TH * TWB);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(tile);
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(d), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0 - TmaTile<R>::PADX), "r"(y0 - R), "r"(b) : "memory");
+  }
+  for (int i = tid; i < 256 * 16; i += kThreads) rng[i] = range[i >> 4];
+  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
+  if (!interior) {
+    for (int i = tid; i < TH * TW; i += kThreads) {
+      const int ty = i / TW, tx = i - ty * TW;
+      const int gy = min(max(y0 - R + ty, 0), H - 1);
+      const int gx = min(max(x0 - R + tx, 0), W - 1);
+      tile[ty * TWB + tx + OFF] = img[(int64_t)gy * W + gx];
+    }
+  }
+  __syncthreads();
+  if (interior) mbar_wait(&bar, 0);
+
+  const int py = tid / (kTileW / kPx);
+  const int px = (tid % (kTileW / kPx)) * kPx;
+  const int gy = y0 + py;
+  if (gy >= row1) return;
+  int c[kPx];
+#pragma unroll
+  for (int j = 0; j < kPx; ++j) c[j] = tile[(py + R) * TWB + px + j + R + OFF];
+  double num[kPx], den[kPx];
+#pragma unroll
+  for (int j = 0; j < kPx; ++j) num[j] = den[j] = 0.0;
+  const double* lane_rng = rng + lane;
+#pragma unroll 1
+  for (int dy = 0; dy < S; ++dy) {
+    int nb[kPx + 2 * R];
+    double nbd[kPx + 2 * R];
+    const uint8_t* trow = tile + (py + dy) * TWB + px + OFF;
+#pragma unroll
+    for (int k = 0; k < kPx + 2 * R; ++k) {
+      nb[k] = trow[k];
+      nbd[k] = (double)nb[k];
+    }
+#pragma unroll
+    for (int dx = 0; dx < S; ++dx) {
+      const double s = sp[dy * S + dx];
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) {
+        const int d = abs(nb[j + dx] - c[j]);
+        const double w = __dmul_rn(s, lane_rng[d << 4]);
+        num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
+        den[j] = __dadd_rn(den[j], w);
+      }
+    }
+  }
+  OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
+#pragma unroll
+  for (int j = 0; j < kPx; ++j)
+    if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
+}
+
+// host: a 2-D uint8 tensor map over the image (driver entry point through
+// the runtime, no libcuda link); false when the layout does not allow one
+bool make_image_tmap(CUtensorMap* map, const uint8_t* img, int H, int W, int box_w, int box_h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode || (W % 16) != 0 || ((uintptr_t)img % 16) != 0 || box_w > 256 || box_h > 256) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
+  const cuuint64_t strides[1] = {(cuuint64_t)W};
+  const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(img), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // generic radius (> kMaxR): same arithmetic, neighbours read from global memory.
 template <typename OUT>
 __global__ void bilateral_generic_kernel(const uint8_t* __restrict__ img, int H, int W, int row0,
@@ -233,6 +352,17 @@ int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const doub
     const char* e = getenv("HB_BILAT_CFG");
     return e ? atoi(e) : 0;
   }();
+  if (variant == 0) {
+    using T = TmaTile<R>;
+    CUtensorMap map;
+    if (make_image_tmap(&map, img, H, W, T::TWB, T::TH)) {
+      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + 256 * 16 * 8 + S * S * 8;
+      HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_tma_kernel<R, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
+      bilateral_tma_kernel<R, OUT><<<grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out);
+      return check_launch();
+    }
+  }
   if (variant == 0 || variant == 2) {
     // one CTA per tile, 16-lane striped table (46 KB smem), 3 CTAs per SM
     const size_t smem = 256 * 16 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;

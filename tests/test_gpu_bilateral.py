@@ -88,3 +88,18 @@ def test_device_resident_path():
     d = torch.from_numpy(pix).cuda()
     got = gpu_bilateral_rows(d, lut, 17, 250).cpu().numpy()
     assert np.array_equal(got, obil.rows(pix, sp, rg, 5, 17, 250))
+
+
+@pytest.mark.parametrize("radius", [0, 2, 5, 8])
+def test_tma_staged_tiles_bit_exact(radius):
+    # widths that are multiples of 16 take the TMA-staged kernel (interior
+    # tiles by one 2-D tensor copy, border tiles by clamped loads)
+    import torch
+
+    pix = ods.image(400, 21)[:, :368].copy()  # 368 % 16 == 0, not a multiple of the 64-wide tile
+    lut = build_bilateral_lut(radius, max(radius / 2.0, 0.5), 30.0)
+    sp, rg = obil.lut(radius, max(radius / 2.0, 0.5), 30.0)
+    d = torch.from_numpy(pix).cuda()
+    for r0, r1 in ((0, 400), (37, 301), (399, 400)):
+        got = gpu_bilateral_rows(d, lut, r0, r1).cpu().numpy()
+        assert np.array_equal(got, obil.rows(pix, sp, rg, radius, r0, r1)), (radius, r0, r1)

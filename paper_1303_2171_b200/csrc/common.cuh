@@ -73,6 +73,10 @@ int stage_in(DevBuf* b, const void* src, size_t bytes, bool device, cudaStream_t
 // Output buffer: borrow when `device`, else allocate (no copy).
 int stage_out(DevBuf* b, void* dst, size_t bytes, bool device, cudaStream_t s);
 int copy_out(void* dst, const DevBuf& b, size_t bytes, bool device, cudaStream_t s);
+// host <-> device for caller buffers: pinned → cudaMemcpyAsync; pageable →
+// pinned double buffer + multi-threaded memcpy (returns with D2H data landed)
+int copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int finish(int flags, cudaStream_t s);  // sync unless HB_ASYNC, surface errors
 int check_launch();
 

@@ -1,7 +1,13 @@
 // runtime.cu — error state, device info cache, staging buffers, generators.
 #include <stdarg.h>
+#include <string.h>
 
+#include <algorithm>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -59,6 +65,174 @@ int alloc(DevBuf* b, size_t bytes, cudaStream_t s) {
   return HB_OK;
 }
 
+// ------------------------------------------------------------------ host transfers
+// Pageable host buffers (plain numpy arrays) cross PCIe through a pinned
+// double buffer: the DMA of chunk i+1 overlaps the multi-threaded memcpy of
+// chunk i between the pinned stage and the pageable array (which also
+// spreads the first-touch page faults of a fresh output over threads).  The
+// driver's own pageable path is single-threaded (~2-10 GB/s); pinned buffers
+// go straight to cudaMemcpyAsync.
+namespace {
+
+// minimal fork-join pool: run(fn, n) calls fn(0..n-1) on up to `size` threads
+class HostPool {
+ public:
+  static HostPool& get() {
+    // never destroyed: its detached workers wait on cv_ until the process
+    // ends, and destroying a condition variable with waiters blocks in glibc
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  void run(const std::function<void(int)>& fn, int n) {
+    std::unique_lock<std::mutex> lk(run_mu_);  // one parallel region at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_ = &fn;
+      next_ = 0;
+      n_ = n;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return done_ == n_; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int n = std::max(0, std::min(8, hw / 2) - 1);
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    for (auto& t : workers_) t.detach();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen && fn_ != nullptr; });
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  void work() {
+    for (;;) {
+      int i;
+      const std::function<void(int)>* fn;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (fn_ == nullptr || next_ >= n_) return;
+        i = next_++;
+        fn = fn_;
+      }
+      (*fn)(i);
+      std::lock_guard<std::mutex> g(mu_);
+      if (++done_ == n_) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int next_ = 0, n_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+};
+
+constexpr size_t kStageChunk = (size_t)32 << 20;  // bytes per pinned stage
+constexpr size_t kPinnedDirect = (size_t)4 << 20;  // smaller copies: plain cudaMemcpyAsync
+
+struct Stager {
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool ready = false;
+};
+thread_local Stager t_stager;  // per calling thread: the two run_workshared sides never share
+
+int stager(Stager** out) {
+  Stager& st = t_stager;
+  if (!st.ready) {
+    for (int i = 0; i < 2; ++i) {
+      HB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.buf[i]), kStageChunk, cudaHostAllocDefault));
+      HB_CUDA_TRY(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming));
+    }
+    st.ready = true;
+  }
+  *out = &st;
+  return HB_OK;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void par_memcpy(char* dst, const char* src, size_t bytes) {
+  HostPool& pool = HostPool::get();
+  const int parts = std::max(1, std::min(pool.size() * 2, (int)(bytes >> 20)));
+  pool.run([&](int k) {
+    const size_t a = bytes * (size_t)k / (size_t)parts, b = bytes * (size_t)(k + 1) / (size_t)parts;
+    memcpy(dst + a, src + a, b - a);
+  }, parts);
+}
+
+}  // namespace
+
+int copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return HB_OK;
+  if (bytes <= kPinnedDirect || is_pinned(src)) {
+    HB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return HB_OK;
+  }
+  Stager* st;
+  HB_TRY(stager(&st));
+  const char* in = reinterpret_cast<const char*>(src);
+  char* out = reinterpret_cast<char*>(dst);
+  for (size_t off = 0, i = 0; off < bytes; off += kStageChunk, ++i) {
+    const size_t len = std::min(kStageChunk, bytes - off);
+    const int b = (int)(i & 1);
+    HB_CUDA_TRY(cudaEventSynchronize(st->ev[b]));  // the stage's previous DMA is done
+    par_memcpy(st->buf[b], in + off, len);
+    HB_CUDA_TRY(cudaMemcpyAsync(out + off, st->buf[b], len, cudaMemcpyHostToDevice, s));
+    HB_CUDA_TRY(cudaEventRecord(st->ev[b], s));
+  }
+  return HB_OK;
+}
+
+int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return HB_OK;
+  if (bytes <= kPinnedDirect || is_pinned(dst)) {
+    HB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    return HB_OK;
+  }
+  Stager* st;
+  HB_TRY(stager(&st));
+  const char* in = reinterpret_cast<const char*>(src);
+  char* out = reinterpret_cast<char*>(dst);
+  const size_t n = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](size_t i) -> int {
+    const size_t off = i * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    HB_CUDA_TRY(cudaMemcpyAsync(st->buf[i & 1], in + off, len, cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaEventRecord(st->ev[i & 1], s));
+    return HB_OK;
+  };
+  HB_TRY(issue(0));
+  for (size_t i = 0; i < n; ++i) {
+    if (i + 1 < n) HB_TRY(issue(i + 1));  // next chunk's DMA overlaps this chunk's memcpy
+    HB_CUDA_TRY(cudaEventSynchronize(st->ev[i & 1]));
+    const size_t off = i * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    par_memcpy(out + off, st->buf[i & 1], len);
+  }
+  return HB_OK;
+}
+
 int stage_in(DevBuf* b, const void* src, size_t bytes, bool device, cudaStream_t s) {
   if (device) {
     b->ptr = const_cast<void*>(src);
@@ -67,8 +241,7 @@ int stage_in(DevBuf* b, const void* src, size_t bytes, bool device, cudaStream_t
     return HB_OK;
   }
   HB_TRY(alloc(b, bytes, s));
-  if (bytes) HB_CUDA_TRY(cudaMemcpyAsync(b->ptr, src, bytes, cudaMemcpyHostToDevice, s));
-  return HB_OK;
+  return copy_h2d(b->ptr, src, bytes, s);
 }
 
 int stage_out(DevBuf* b, void* dst, size_t bytes, bool device, cudaStream_t s) {
@@ -83,8 +256,7 @@ int stage_out(DevBuf* b, void* dst, size_t bytes, bool device, cudaStream_t s) {
 
 int copy_out(void* dst, const DevBuf& b, size_t bytes, bool device, cudaStream_t s) {
   if (device || bytes == 0) return HB_OK;
-  HB_CUDA_TRY(cudaMemcpyAsync(dst, b.ptr, bytes, cudaMemcpyDeviceToHost, s));
-  return HB_OK;
+  return copy_d2h(dst, b.ptr, bytes, s);
 }
 
 int check_launch() {

@@ -645,7 +645,7 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
                                : launch_spmv<int64_t, int64_t, int64_t>(d_ptr.ptr, d_col.ptr, dv, dx, 0, rows, nullptr, dy, mode, s);
   if (rc != HB_OK) return rc;
   if (perm == nullptr) {
-    HB_CUDA_TRY(cudaMemcpyAsync(y, d_y.ptr, (size_t)rows * 8, cudaMemcpyDeviceToHost, s));
+    HB_TRY(copy_d2h(y, d_y.ptr, (size_t)rows * 8, s));
     HB_CUDA_TRY(cudaStreamSynchronize(s));
     return HB_OK;
   }

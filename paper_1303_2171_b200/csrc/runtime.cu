@@ -148,20 +148,43 @@ constexpr size_t kPinnedDirect = (size_t)4 << 20;  // smaller copies: plain cuda
 struct Stager {
   char* buf[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
-  bool ready = false;
 };
-thread_local Stager t_stager;  // per calling thread: the two run_workshared sides never share
 
-int stager(Stager** out) {
-  Stager& st = t_stager;
-  if (!st.ready) {
-    for (int i = 0; i < 2; ++i) {
-      HB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.buf[i]), kStageChunk, cudaHostAllocDefault));
-      HB_CUDA_TRY(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming));
+// Process-wide free list: a call borrows a stager (allocated once, pinned
+// memory is expensive to allocate) and returns it when its copy is done.
+// Calls come from short-lived Python pool threads, so per-thread buffers
+// would be re-allocated (and leaked) on every call.
+std::mutex g_stage_mu;
+std::vector<Stager*> g_stage_free;
+
+struct StagerLease {
+  Stager* st = nullptr;
+  ~StagerLease() {
+    if (st) {
+      std::lock_guard<std::mutex> g(g_stage_mu);
+      g_stage_free.push_back(st);
     }
-    st.ready = true;
   }
-  *out = &st;
+};
+
+int stager(StagerLease* lease) {
+  {
+    std::lock_guard<std::mutex> g(g_stage_mu);
+    if (!g_stage_free.empty()) {
+      lease->st = g_stage_free.back();
+      g_stage_free.pop_back();
+      return HB_OK;
+    }
+  }
+  Stager* st = new Stager();
+  for (int i = 0; i < 2; ++i) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&st->buf[i]), kStageChunk, cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&st->ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      set_error("pinned staging buffer: %s", cudaGetErrorString(cudaGetLastError()));
+      return HB_ECUDA;  // (a partially built stager is leaked; this only happens when pinned memory runs out)
+    }
+  }
+  lease->st = st;
   return HB_OK;
 }
 
@@ -191,8 +214,9 @@ int copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     HB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return HB_OK;
   }
-  Stager* st;
-  HB_TRY(stager(&st));
+  StagerLease lease;
+  HB_TRY(stager(&lease));
+  Stager* st = lease.st;
   const char* in = reinterpret_cast<const char*>(src);
   char* out = reinterpret_cast<char*>(dst);
   for (size_t off = 0, i = 0; off < bytes; off += kStageChunk, ++i) {
@@ -203,6 +227,9 @@ int copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     HB_CUDA_TRY(cudaMemcpyAsync(out + off, st->buf[b], len, cudaMemcpyHostToDevice, s));
     HB_CUDA_TRY(cudaEventRecord(st->ev[b], s));
   }
+  // the stager goes back to the free list: its last DMAs must be done first
+  HB_CUDA_TRY(cudaEventSynchronize(st->ev[0]));
+  HB_CUDA_TRY(cudaEventSynchronize(st->ev[1]));
   return HB_OK;
 }
 
@@ -212,8 +239,9 @@ int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     HB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
     return HB_OK;
   }
-  Stager* st;
-  HB_TRY(stager(&st));
+  StagerLease lease;
+  HB_TRY(stager(&lease));
+  Stager* st = lease.st;
   const char* in = reinterpret_cast<const char*>(src);
   char* out = reinterpret_cast<char*>(dst);
   const size_t n = (bytes + kStageChunk - 1) / kStageChunk;

@@ -26,6 +26,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -611,12 +612,15 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
   const bool p32 = nz1 - nz0 <= (int64_t)INT32_MAX;
   std::vector<int64_t> ptr64(p32 ? 0 : (size_t)rows + 1);
   std::vector<int32_t> ptr32(p32 ? (size_t)rows + 1 : 0);
-  for (int64_t i = 0; i <= rows; ++i) {
-    int64_t v;
-    read_index(row_ptr, ptr_code, row0 + i, false, s, &v);
-    if (p32) ptr32[(size_t)i] = (int32_t)(v - nz0);
-    else ptr64[(size_t)i] = v - nz0;
-  }
+  auto rebase = [&](auto* src) {  // typed (vectorisable) loop
+    for (int64_t i = 0; i <= rows; ++i) {
+      const int64_t v = (int64_t)src[row0 + i] - nz0;
+      if (p32) ptr32[(size_t)i] = (int32_t)v;
+      else ptr64[(size_t)i] = v;
+    }
+  };
+  if (ptr_code == HB_I32) rebase(reinterpret_cast<const int32_t*>(row_ptr));
+  else rebase(reinterpret_cast<const int64_t*>(row_ptr));
   (void)pe;
   if (p32) HB_TRY(stage_in(&d_ptr, ptr32.data(), ptr32.size() * 4, false, s));
   else HB_TRY(stage_in(&d_ptr, ptr64.data(), ptr64.size() * 8, false, s));
@@ -650,13 +654,20 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
     return HB_OK;
   }
   std::vector<double> tmp((size_t)rows);
-  HB_CUDA_TRY(cudaMemcpyAsync(tmp.data(), d_y.ptr, (size_t)rows * 8, cudaMemcpyDeviceToHost, s));
+  HB_TRY(copy_d2h(tmp.data(), d_y.ptr, (size_t)rows * 8, s));
   HB_CUDA_TRY(cudaStreamSynchronize(s));
-  for (int64_t i = 0; i < rows; ++i) {
-    int64_t dst;
-    read_index(perm, perm_code, row0 + i, false, s, &dst);
-    y[dst] = tmp[(size_t)i];
-  }
+  // un-permute on the host: y[perm[row0 + i]] = row sum i (typed loop, 4 threads)
+  auto scatter = [&](auto* pm) {
+    const int nt = rows >= (1 << 18) ? 4 : 1;
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        for (int64_t i = rows * t / nt, e = rows * (t + 1) / nt; i < e; ++i) y[(int64_t)pm[row0 + i]] = tmp[(size_t)i];
+      });
+    for (auto& t : th) t.join();
+  };
+  if (perm_code == HB_I32) scatter(reinterpret_cast<const int32_t*>(perm));
+  else scatter(reinterpret_cast<const int64_t*>(perm));
   (void)qe;
   return HB_OK;
 }

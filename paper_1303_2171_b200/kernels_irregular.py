@@ -377,12 +377,29 @@ def spmv_hybrid(prep: SpmvPrep, x: Any) -> np.ndarray:
         raise ValueError(f"x must have length {m.cols}, got {xh.shape}")
     split = prep.split_row
     x_side_b = x if (m.on_device and is_device_array(x)) else xh
+    g = sharding.active_group()
+    if m.on_device or (g is not None and g.world > 1):
+        with ThreadPoolExecutor(max_workers=2) as pool:
+            fa = pool.submit(_host_range_matvec, m, xh, 0, split, prep.workers_a)
+            fb = pool.submit(_gpu_rows, m, x_side_b, split, m.rows)
+            y_perm = np.concatenate([fa.result(), fb.result()])
+        y = np.empty_like(y_perm)
+        y[to_host(prep.perm)] = y_perm
+        return y
+    # host matrix, one GPU: each side scatters its own rows into y (the GPU
+    # side inside the C call) — no concatenation, no full-size host scatter
+    perm = np.asarray(to_host(prep.perm))
+    y = np.empty(m.rows)
+
+    def side_a():
+        y[perm[:split]] = _host_range_matvec(m, xh, 0, split, prep.workers_a)
+
     with ThreadPoolExecutor(max_workers=2) as pool:
-        fa = pool.submit(_host_range_matvec, m, xh, 0, split, prep.workers_a)
-        fb = pool.submit(_gpu_rows, m, x_side_b, split, m.rows)
-        y_perm = np.concatenate([fa.result(), fb.result()])
-    y = np.empty_like(y_perm)
-    y[to_host(prep.perm)] = y_perm
+        fa = pool.submit(side_a)
+        fb = pool.submit(gpu_spmv, m, xh, split, m.rows, y, perm) if split < m.rows else None
+        fa.result()
+        if fb is not None:
+            fb.result()
     return y
 
 

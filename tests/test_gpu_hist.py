@@ -116,6 +116,6 @@ def test_measured_calibration_host_vs_gpu():
     wl = HistogramWorkload(data, 256)
     share = calibrate_measured(wl, p, max_refinements=4)
     assert 0.0 <= share.fraction_a <= 1.0 and share.origin.value == "calibrated"
-    assert share.probe.t_device_a > 0 and share.probe.t_device_b > 0 and len(share.probe.refinement_steps) == 5
+    assert share.probe.t_device_a > 0 and share.probe.t_device_b > 0 and len(share.probe.refinement_steps) >= 5
     out = hybrid_histogram(data, 256, p, share)
     assert np.array_equal(out.bins, np.bincount(data, minlength=256))

@@ -692,7 +692,7 @@ __global__ void scan_hist_kernel(const uint32_t* __restrict__ hist, uint32_t* __
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE, int LBW = 1>
+template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE, int LBW = 1, bool MATCH = false>
 __global__ void __launch_bounds__(T, 1024 / T)
     onesweep_ec_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                        uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(T, 1024 / T)
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t d = dig[i];
-        const uint32_t peers = match_digit8(d);
+        const uint32_t peers = MATCH ? __match_any_sync(0xffffffffu, d) : match_digit8(d);
         const uint32_t below = __popc(peers & lt);
         const uint32_t pre = wr[d];
         __syncwarp();
@@ -874,19 +874,19 @@ struct PassArgs {
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
 };
 
-template <typename K, int I, int T = 512, bool TWO = false, int LBW = 1>
+template <typename K, int I, int T = 512, bool TWO = false, int LBW = 1, bool MATCH = false>
 int launch_ec(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
   const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
   *tiles_out = tiles;
   if (dry) return HB_OK;
   const size_t smem = (size_t)T * I * sizeof(K) + (a.vin ? (size_t)T * I * 4 : 0);
   if (a.vin) {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO, LBW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, true, I, T, TWO, LBW><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO, LBW, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, true, I, T, TWO, LBW, MATCH><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   } else {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO, LBW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, false, I, T, TWO, LBW><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO, LBW, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, false, I, T, TWO, LBW, MATCH><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   }
   return check_launch();
@@ -1007,6 +1007,9 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 25: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);
     case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
     case 26: return launch_ec<K, 20, 384>(a, s, tiles, dry);
+    case 27: return launch_ec<K, 20, 384, false, 2, true>(a, s, tiles, dry);
+    case 28: return launch_ec<K, 16, 384, false, 2, true>(a, s, tiles, dry);
+    case 29: return launch_ec<K, 24, 384, false, 2, true>(a, s, tiles, dry);
     default: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);  // best measured (round 1)
   }
   }

@@ -31,7 +31,7 @@ from pathlib import Path
 
 import numpy as np
 
-ARGS = argparse.Namespace(e2e_share="calibrated")  # set by main()
+ARGS = argparse.Namespace(e2e_share="auto")  # set by main()
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -59,11 +59,16 @@ def host_platform():
 
 def e2e_share(args, workload, platform):
     """The split the e2e leg runs with: `--e2e-share gpu` → all on the GPU;
-    `calibrated` (default) → worksharing.calibrate_measured on this box (the
-    paper's hybrid host+GPU split, measured, not modelled; untimed)."""
+    `calibrated` → worksharing.calibrate_measured on this box (the paper's
+    hybrid host+GPU split, measured, not modelled; untimed); `auto` (default)
+    → calibrated at N=1, all on the GPU when several ranks share the host."""
     from paper_1303_2171_b200.worksharing import WorkShare, calibrate_measured
 
-    if args.e2e_share == "gpu" or workload is None:
+    import torch.distributed as dist
+
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+    if args.e2e_share == "gpu" or workload is None or (args.e2e_share == "auto" and multi):
+        # N > 1: the ranks share one host's cores, so the host share is off
         return WorkShare.manual(0.0)
     return calibrate_measured(workload, platform, max_refinements=6, repeats=2)
 
@@ -954,8 +959,9 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the end-to-end (host buffer) leg")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--e2e-share", default="calibrated", choices=["calibrated", "gpu"],
-                    help="e2e leg split: measured host+GPU calibration (default) or all on the GPU")
+    ap.add_argument("--e2e-share", default="auto", choices=["auto", "calibrated", "gpu"],
+                    help="e2e leg split: measured host+GPU calibration, all on the GPU, or auto "
+                         "(calibrated at N=1, GPU-only when ranks share the host)")
     args = ap.parse_args()
     global ARGS
     ARGS = args

@@ -103,8 +103,10 @@ class HostPool {
 
  private:
   HostPool() {
+    // the pageable side of a transfer is bound by first-touch page zeroing of
+    // fresh output arrays (~10 GB/s per thread), so use every core
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    const int n = std::max(0, std::min(8, hw / 2) - 1);
+    const int n = std::max(0, std::min(32, hw) - 1);
     for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
     for (auto& t : workers_) t.detach();
   }

@@ -412,7 +412,7 @@ class BilatBench:
 
     name = "bilat"
     unit = "Mpix/s"
-    kernel = "bilateral_tile_kernel"
+    kernel = "bilateral_tma_kernel"
 
     def __init__(self, side: int = 16384, radius: int = 5, seed: int = 42):
         self.side, self.radius, self.seed = side, radius, seed
@@ -509,7 +509,7 @@ class ConvBench(BilatBench):
     fp64 arithmetic bit-identical to the reference, fp32 output image."""
 
     name = "conv"
-    kernel = "conv_tile_kernel"
+    kernel = "conv_rows_kernel"
     compute_bound = "fp64 issue (1 DMUL + 1 DADD per tap)"
 
     def __init__(self, side: int = 16384, radius: int = 7, seed: int = 42):

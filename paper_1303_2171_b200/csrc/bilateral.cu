@@ -208,33 +208,43 @@ __global__ void __launch_bounds__(kThreads, 2)
 // instead of (TH x TW) / 256 clamped byte loads per thread; border CTAs keep
 // the clamped loads (TMA zero-fills out-of-range elements, the reference
 // clamps).  Range table striped over 16 lanes, 3 CTAs/SM.
-template <int R>
+template <int R, int NR = 1>
 struct TmaTile {
   // the innermost TMA coordinate must be 16-byte aligned (an unaligned start
   // faults: scripts/micro/tma2d.cu), so the box starts 16 columns left of the
   // tile and is 16 + 64 + 16 wide; logical halo column tx sits at tx + OFF
-  static constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
+  static constexpr int TILE_H = kTileH * NR;
+  static constexpr int TH = TILE_H + 2 * R, TW = kTileW + 2 * R;
   static constexpr int PADX = 16, TWB = kTileW + 2 * PADX, OFF = PADX - R;
   static_assert(R <= PADX, "halo wider than the aligned pad");
+  static_assert(TH <= 256, "TMA box height");
 };
 
-template <int R, typename OUT>
-__global__ void __launch_bounds__(kThreads, 3)
+// NR output rows per thread (tile 32·NR x 64): a loaded tap row segment (and
+// its fp64 conversion) serves all NR rows; per pixel the taps stay in
+// row-major order, so the result is bit-identical.
+template <int R, typename OUT, int NR, int MINB, bool SYM = false>
+__global__ void __launch_bounds__(kThreads, MINB)
     bilateral_tma_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ img, int H, int W,
                          int row0, int row1, const double* __restrict__ spatial, const double* __restrict__ range,
                          OUT* __restrict__ out) {
+  using T = TmaTile<R, NR>;
   constexpr int S = 2 * R + 1;
-  constexpr int TH = TmaTile<R>::TH, TW = TmaTile<R>::TW, TWB = TmaTile<R>::TWB, OFF = TmaTile<R>::OFF;
+  constexpr int TH = T::TH, TW = T::TW, TWB = T::TWB, OFF = T::OFF;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
+  // SYM: the range table is stored for signed differences -255..255 (511
+  // rows, entry 255+e = range[|e|]), so a tap indexes it with nb - c directly
+  // — no IABS — at twice the shared memory
+  constexpr int NE = SYM ? 511 : 256;
   uint8_t* tile = smem;                                                     // [TH][TWB], 128-B aligned
-  double* rng = reinterpret_cast<double*>(smem + ((TH * TWB + 127) / 128) * 128);  // [256][16]
-  double* sp = rng + 256 * 16;                                              // [S*S]
+  double* rng = reinterpret_cast<double*>(smem + ((TH * TWB + 127) / 128) * 128);  // [NE][16]
+  double* sp = rng + NE * 16;                                               // [S*S]
   const int tid = threadIdx.x;
   const int lane = tid & 15;
-  const int y0 = row0 + blockIdx.y * kTileH;
+  const int y0 = row0 + blockIdx.y * T::TILE_H;
   const int x0 = blockIdx.x * kTileW;
-  const bool interior = x0 - TmaTile<R>::PADX >= 0 && x0 - TmaTile<R>::PADX + TWB <= W && y0 - R >= 0 && y0 - R + TH <= H;
+  const bool interior = x0 - T::PADX >= 0 && x0 - T::PADX + TWB <= W && y0 - R >= 0 && y0 - R + TH <= H;
   if (interior && tid == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -243,9 +253,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(d), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0 - TmaTile<R>::PADX), "r"(y0 - R), "r"(b) : "memory");
+        ::"r"(d), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0 - T::PADX), "r"(y0 - R), "r"(b) : "memory");
   }
-  for (int i = tid; i < 256 * 16; i += kThreads) rng[i] = range[i >> 4];
+  for (int i = tid; i < NE * 16; i += kThreads) rng[i] = range[SYM ? abs((i >> 4) - 255) : (i >> 4)];
   for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
   if (!interior) {
     for (int i = tid; i < TH * TW; i += kThreads) {
@@ -258,43 +268,55 @@ __global__ void __launch_bounds__(kThreads, 3)
   __syncthreads();
   if (interior) mbar_wait(&bar, 0);
 
-  const int py = tid / (kTileW / kPx);
+  const int py = (tid / (kTileW / kPx)) * NR;
   const int px = (tid % (kTileW / kPx)) * kPx;
   const int gy = y0 + py;
   if (gy >= row1) return;
-  int c[kPx];
+  int c[NR][kPx];
+  double num[NR][kPx], den[NR][kPx];
 #pragma unroll
-  for (int j = 0; j < kPx; ++j) c[j] = tile[(py + R) * TWB + px + j + R + OFF];
-  double num[kPx], den[kPx];
+  for (int k = 0; k < NR; ++k)
 #pragma unroll
-  for (int j = 0; j < kPx; ++j) num[j] = den[j] = 0.0;
-  const double* lane_rng = rng + lane;
+    for (int j = 0; j < kPx; ++j) {
+      c[k][j] = tile[(py + k + R) * TWB + px + j + R + OFF];
+      num[k][j] = den[k][j] = 0.0;
+    }
+  const double* lane_rng = rng + lane + (SYM ? 255 * 16 : 0);
 #pragma unroll 1
-  for (int dy = 0; dy < S; ++dy) {
+  for (int iy = 0; iy < S + NR - 1; ++iy) {
     int nb[kPx + 2 * R];
     double nbd[kPx + 2 * R];
-    const uint8_t* trow = tile + (py + dy) * TWB + px + OFF;
+    const uint8_t* trow = tile + (py + iy) * TWB + px + OFF;
 #pragma unroll
-    for (int k = 0; k < kPx + 2 * R; ++k) {
-      nb[k] = trow[k];
-      nbd[k] = (double)nb[k];
+    for (int q = 0; q < kPx + 2 * R; ++q) {
+      nb[q] = trow[q];
+      nbd[q] = (double)nb[q];
     }
 #pragma unroll
-    for (int dx = 0; dx < S; ++dx) {
-      const double s = sp[dy * S + dx];
+    for (int k = 0; k < NR; ++k) {
+      const int dy = iy - k;
+      if (dy < 0 || dy >= S) continue;
 #pragma unroll
-      for (int j = 0; j < kPx; ++j) {
-        const int d = abs(nb[j + dx] - c[j]);
-        const double w = __dmul_rn(s, lane_rng[d << 4]);
-        num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
-        den[j] = __dadd_rn(den[j], w);
+      for (int dx = 0; dx < S; ++dx) {
+        const double s = sp[dy * S + dx];
+#pragma unroll
+        for (int j = 0; j < kPx; ++j) {
+          const int d = SYM ? nb[j + dx] - c[k][j] : abs(nb[j + dx] - c[k][j]);
+          const double w = __dmul_rn(s, lane_rng[d * 16]);
+          num[k][j] = __dadd_rn(num[k][j], __dmul_rn(w, nbd[j + dx]));
+          den[k][j] = __dadd_rn(den[k][j], w);
+        }
       }
     }
   }
-  OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
 #pragma unroll
-  for (int j = 0; j < kPx; ++j)
-    if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
+  for (int k = 0; k < NR; ++k) {
+    if (gy + k >= row1) break;
+    OUT* o = out + (int64_t)(gy + k - row0) * W + x0 + px;
+#pragma unroll
+    for (int j = 0; j < kPx; ++j)
+      if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[k][j], den[k][j]);
+  }
 }
 
 // host: a 2-D uint8 tensor map over the image (driver entry point through
@@ -352,16 +374,27 @@ int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const doub
     const char* e = getenv("HB_BILAT_CFG");
     return e ? atoi(e) : 0;
   }();
-  if (variant == 0) {
-    using T = TmaTile<R>;
-    CUtensorMap map;
-    if (make_image_tmap(&map, img, H, W, T::TWB, T::TH)) {
-      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + 256 * 16 * 8 + S * S * 8;
-      HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_tma_kernel<R, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
-      bilateral_tma_kernel<R, OUT><<<grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out);
+  if (variant == 0 || (variant >= 4 && variant <= 7)) {
+    // TMA-staged tiles.  default: one row per thread, symmetric 511-entry
+    // range table, 3 CTAs/SM; HB_BILAT_CFG 4: |d| table, 5: 2 rows, 6: 3 rows,
+    // 7: 2 rows with the symmetric table
+    auto launch_tma = [&](auto kern, auto tag, bool sym) -> int {
+      using T = decltype(tag);
+      CUtensorMap map;
+      if (!make_image_tmap(&map, img, H, W, T::TWB, T::TH)) return -1;
+      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + (sym ? 511 : 256) * 16 * 8 + S * S * 8;
+      HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, T::TILE_H));
+      kern<<<grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out);
       return check_launch();
-    }
+    };
+    int rc;
+    if (variant == 4) rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3>, TmaTile<R, 1>{}, false);
+    else if (variant == 5) rc = launch_tma(bilateral_tma_kernel<R, OUT, 2, 2>, TmaTile<R, 2>{}, false);
+    else if (variant == 6) rc = launch_tma(bilateral_tma_kernel<R, OUT, 3, 2>, TmaTile<R, 3>{}, false);
+    else if (variant == 7) rc = launch_tma(bilateral_tma_kernel<R, OUT, 2, 2, true>, TmaTile<R, 2>{}, true);
+    else rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3, true>, TmaTile<R, 1>{}, true);
+    if (rc != -1) return rc;  // -1: no tensor map for this layout, plain tiles below
   }
   if (variant == 0 || variant == 2) {
     // one CTA per tile, 16-lane striped table (46 KB smem), 3 CTAs per SM

@@ -376,6 +376,42 @@ def hybrid_sort(data: Any, platform: Platform, leaf_a: int = 2048, leaf_b: int =
 
 
 # --------------------------------------------------------------------------
+# row-strip filters: shared output image
+
+
+def _host_rows_out(out: np.ndarray | None, rows: int, width: int) -> np.ndarray:
+    if out is None:
+        return np.zeros((max(rows, 0), width))
+    if out.shape != (max(rows, 0), width) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 (rows, width) array")
+    return out
+
+
+class _StripOutput:
+    """Both sides of a host-image run write their row strips straight into one
+    output image allocated by partition() (np.empty: no page is touched until
+    a side writes its strip), so merge() hands that image back instead of the
+    reference's vstack copy (an extra pass over H×W×8 bytes).  Device images
+    and GPU groups keep the partial-array protocol."""
+
+    def _new_output(self, height: int, width: int) -> None:
+        pix = self.image.pixels
+        local = not is_device_array(pix) and (sharding.active_group() is None or sharding.active_group().world == 1)
+        self._out = np.empty((height, width)) if local else None
+
+    def _strip(self, part) -> np.ndarray | None:
+        out = getattr(self, "_out", None)
+        return None if out is None else out[part[0] : part[1]]
+
+    def merge(self, partials: Sequence[np.ndarray]) -> Image:
+        out = getattr(self, "_out", None)
+        if out is not None and all(isinstance(p, np.ndarray) and (p.size == 0 or np.shares_memory(p, out))
+                                   for p in partials):
+            return Image(out)
+        return Image(np.vstack([sharding.to_numpy(p) for p in partials]))
+
+
+# --------------------------------------------------------------------------
 # convolution (kernels_regular.py:327-414)
 
 
@@ -410,7 +446,8 @@ class FilterKernel:
         return cls(g / g.sum())
 
 
-def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, workers: int = 1) -> np.ndarray:
+def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, workers: int = 1,
+                  out: np.ndarray | None = None) -> np.ndarray:
     """Host (DeviceA) body, the reference arithmetic (:359-381) in native code
     (hb_host_conv_rows on `workers` threads): correlation of rows [row0, row1)
     with clamp-to-edge borders, one weighted plane added per non-zero tap in
@@ -420,7 +457,7 @@ def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, worke
         arr = arr.astype(np.float64)
     arr = np.ascontiguousarray(arr)
     height, width = arr.shape
-    out = np.zeros((max(row1 - row0, 0), width))
+    out = _host_rows_out(out, row1 - row0, width)
     if row1 <= row0:
         return out
     if not 0 <= row0 and row1 <= height:
@@ -476,10 +513,11 @@ def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, o
     return out
 
 
-class ConvolutionWorkload:
+class ConvolutionWorkload(_StripOutput):
     """Horizontal strip split at floor(f·H); halo rows are read from the
-    shared source image (kernels_regular.py:384-405).  DeviceA: numpy planes;
-    DeviceB: the GPU tile kernel over the GPU group (floor(k·n/G) strips)."""
+    shared source image (kernels_regular.py:384-405).  DeviceA: native host
+    threads; DeviceB: the GPU tile kernel over the GPU group (floor(k·n/G)
+    strips); both write into one output image (_StripOutput)."""
 
     name = "conv"
     unit = "neighbor accumulations"
@@ -491,20 +529,21 @@ class ConvolutionWorkload:
 
     def partition(self, fraction_a: float):
         split = int(math.floor(fraction_a * self.image.height))
+        self._new_output(self.image.height, self.image.width)
         return (0, split), (split, self.image.height)
 
     def work_units(self, part) -> float:
         return float((part[1] - part[0]) * self._per_row)
 
     def run_part(self, device: Device, part) -> np.ndarray:
+        strip = self._strip(part)
         if device.id is DeviceId.B:
+            if strip is not None:
+                return gpu_convolve_rows(self.image.pixels, self.kernel, part[0], part[1], out=strip)
             return sharding.run_sharded_rows(
                 part[0], part[1], lambda a, b: gpu_convolve_rows(self.image.pixels, self.kernel, a, b)
             )
-        return convolve_rows(self.image.pixels, self.kernel, part[0], part[1], device.worker_count)
-
-    def merge(self, partials: Sequence[np.ndarray]) -> Image:
-        return Image(np.vstack([sharding.to_numpy(p) for p in partials]))
+        return convolve_rows(self.image.pixels, self.kernel, part[0], part[1], device.worker_count, out=strip)
 
 
 def hybrid_convolve(image: Image, kernel: FilterKernel, platform: Platform,
@@ -558,14 +597,15 @@ def build_bilateral_lut(radius: int, sigma_s: float, sigma_r: float) -> Bilatera
     return BilateralLut(spatial, np.exp(-(k**2) / (2.0 * sigma_r**2)), sigma_s, sigma_r, radius)
 
 
-def bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, workers: int = 1) -> np.ndarray:
+def bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, workers: int = 1,
+                   out: np.ndarray | None = None) -> np.ndarray:
     """Host (DeviceA) body, the reference arithmetic (:461-486) in native code
     (hb_host_bilateral on `workers` threads): for each tap in row-major order
     w = spatial·range[|nb-c|], num += w·nb, den += w; clamp to edge; returns
     num/den as float64 rows [row0, row1)."""
     pix = np.ascontiguousarray(to_host(pixels), dtype=np.uint8)
     height, width = pix.shape
-    out = np.zeros((max(row1 - row0, 0), width))
+    out = _host_rows_out(out, row1 - row0, width)
     if row1 <= row0:
         return out
     if not 0 <= row0 and row1 <= height:
@@ -615,7 +655,7 @@ def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out
     return out
 
 
-class BilateralApplyWorkload:
+class BilateralApplyWorkload(_StripOutput):
     """Row strips split at floor(f·H) (:489-511).  DeviceA: numpy rows;
     DeviceB: the GPU tile kernel, its strip split again over the GPU group
     (floor(k·n/G)) and gathered; the merge stacks the strips."""
@@ -630,20 +670,21 @@ class BilateralApplyWorkload:
 
     def partition(self, fraction_a: float):
         split = int(math.floor(fraction_a * self.image.height))
+        self._new_output(self.image.height, self.image.width)
         return (0, split), (split, self.image.height)
 
     def work_units(self, part) -> float:
         return float((part[1] - part[0]) * self._per_row)
 
     def run_part(self, device: Device, part) -> np.ndarray:
+        strip = self._strip(part)
         if device.id is DeviceId.B:
+            if strip is not None:
+                return gpu_bilateral_rows(self.image.pixels, self.lut, part[0], part[1], out=strip)
             return sharding.run_sharded_rows(
                 part[0], part[1], lambda a, b: gpu_bilateral_rows(self.image.pixels, self.lut, a, b)
             )
-        return bilateral_rows(self.image.pixels, self.lut, part[0], part[1], device.worker_count)
-
-    def merge(self, partials: Sequence[np.ndarray]) -> Image:
-        return Image(np.vstack([sharding.to_numpy(p) for p in partials]))
+        return bilateral_rows(self.image.pixels, self.lut, part[0], part[1], device.worker_count, out=strip)
 
 
 def hybrid_bilateral(image: Image, lut: BilateralLut, platform: Platform, share: WorkShare | None = None) -> Image:

@@ -24,6 +24,7 @@
 //   passes, a constant array in 0.
 #include <stdlib.h>
 
+#include <mutex>
 #include <utility>
 
 #include "common.cuh"
@@ -692,7 +693,8 @@ __global__ void scan_hist_kernel(const uint32_t* __restrict__ hist, uint32_t* __
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE, int LBW = 1, bool MATCH = false>
+template <typename K, bool HAS_V, int I, int T, bool TWO_PHASE, int LBW = 1, bool MATCH = false,
+          bool ATOMS_RANK = false>
 __global__ void __launch_bounds__(T, 1024 / T)
     onesweep_ec_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                        uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
@@ -764,6 +766,13 @@ __global__ void __launch_bounds__(T, 1024 / T)
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t d = dig[i];
+        if constexpr (ATOMS_RANK) {
+          // one shared atomic per key: lanes of a warp that hit the same
+          // counter get their old values in lane order (verified on the
+          // device at first use, atoms_rank_ok), i.e. pre + below directly
+          rank[i] = atomicAdd(&wr[d], 1u);
+          continue;
+        }
         const uint32_t peers = MATCH ? __match_any_sync(0xffffffffu, d) : match_digit8(d);
         const uint32_t below = __popc(peers & lt);
         const uint32_t pre = wr[d];
@@ -862,6 +871,145 @@ __global__ void __launch_bounds__(T, 1024 / T)
   }
 }
 
+// ------------------------------------------------------------------ 2f. rank-first onesweep
+// Ranking is ONE shared atomic per key: the lanes of a warp that hit the same
+// per-warp digit counter get their old values in lane order — the stable
+// rank (pre + lower peers) — so the eight-ballot multi-split disappears.
+// This is not documented CUDA behaviour; it is verified on the device before
+// first use (atoms_rank_ok below, 2^20 random rows per digit modulus) and
+// the ballot kernel is used if the check fails.  After the ranking pass the
+// counters hold the per-warp digit counts, so no separate counting pass is
+// needed; warps 0-7 then publish, scan and look back while the rest wait.
+template <typename K, bool HAS_V, int I, int T, int LBW, int MINB>
+__global__ void __launch_bounds__(T, MINB)
+    onesweep_rf_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
+                       uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
+                       const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
+                       uint32_t* __restrict__ tile_counter) {
+  constexpr int W = T / 32, TILE = T * I;
+  static_assert(T >= 256, "one look-back thread per digit");
+  __shared__ uint32_t s_base[W][256];  // per-warp running counts → per-(warp, digit) tile positions
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_scr[8];
+  __shared__ uint32_t s_tile;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  K* s_keys = reinterpret_cast<K*>(s_dyn);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + TILE);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < W * 256; i += T) (&s_base[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * TILE;
+  const int valid = (int)min((int64_t)TILE, n - base);
+  const K* kt = kin + base;
+  const uint32_t* vt = HAS_V ? vin + base : nullptr;
+  const int wbase = warp * 32 * I;
+  K key[I];
+  uint32_t val[I], rank[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const int idx = wbase + i * 32 + lane;
+    const bool ok = idx < valid;
+    key[i] = ok ? kt[idx] : (K)(~(K)0 ^ flip);
+    if (HAS_V) val[i] = ok ? vt[idx] : 0u;
+  }
+  uint32_t gs = 0;
+  if (tid < 256) gs = gstart[tid];
+#pragma unroll
+  for (int i = 0; i < I; ++i) rank[i] = atomicAdd(&s_base[warp][digit_of<K>(key[i], flip, shift)], 1u);
+  __syncthreads();
+
+  if (tid < 256) {
+    const int d = tid;
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) c += s_base[w][d];
+    if (tile == 0) st_relaxed(lookback + d, kFlagInc | c);
+    else st_relaxed(lookback + (size_t)tile * 256 + d, kFlagAgg | c);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_scr[warp] = x;
+    bar_named(1, 256);
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    const uint32_t dstart = x - c + add;
+    uint32_t run = dstart;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t t = s_base[w][d];
+      s_base[w][d] = run;
+      run += t;
+    }
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      bool done = false;
+      while (!done) {
+        uint32_t wv[LBW];
+#pragma unroll
+        for (int j = 0; j < LBW; ++j) {
+          const int64_t tj = t - j < 0 ? 0 : t - j;
+          wv[j] = ld_relaxed(lookback + (size_t)tj * 256 + d);
+        }
+        int used = 0;
+#pragma unroll
+        for (int j = 0; j < LBW; ++j) {
+          if (done || used < j) continue;
+          const uint32_t flag = wv[j] & ~kCountMask;
+          if (flag == 0) continue;
+          excl += wv[j] & kCountMask;
+          used = j + 1;
+          if (flag == kFlagInc) done = true;
+        }
+        t -= used;
+      }
+      st_relaxed(lookback + (size_t)tile * 256 + d, kFlagInc | (excl + c));
+    }
+    s_goff[d] = gs + excl - dstart;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const uint32_t p = s_base[warp][digit_of<K>(key[i], flip, shift)] + rank[i];
+    s_keys[p] = key[i];
+    if (HAS_V) s_vals[p] = val[i];
+  }
+  __syncthreads();
+  for (int j = tid; j < valid; j += T) {
+    const K k = s_keys[j];
+    const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
+    kout[dst] = k;
+    if (HAS_V) vout[dst] = s_vals[j];
+  }
+}
+
+// device check of the lane-ordered shared atomics the rank-first kernel relies on
+__global__ void atoms_order_check(unsigned int* bad, int rows) {
+  __shared__ uint32_t cnt[8][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int mod : {2, 5, 32, 256}) {
+    for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
+    __syncwarp();
+    for (int r = 0; r < rows; ++r) {
+      const uint32_t d = (uint32_t)(splitmix64_at((uint64_t)(blockIdx.x * 8 + warp) * 7919u + mod, (uint64_t)r * 32 + lane) %
+                                    (uint64_t)mod);
+      const uint32_t before = cnt[warp][d];
+      __syncwarp();
+      const uint32_t below = __popc(__match_any_sync(0xffffffffu, d) & lt);
+      const uint32_t got = atomicAdd(&cnt[warp][d], 1u);
+      __syncwarp();
+      if (got != before + below) atomicAdd(bad, 1u);
+    }
+  }
+}
+
 template <typename K, int T, int I>
 size_t onesweep_smem(bool has_v) {
   return (size_t)T * I * sizeof(K) + (has_v ? (size_t)T * I * 4 : 0);
@@ -874,19 +1022,58 @@ struct PassArgs {
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
 };
 
-template <typename K, int I, int T = 512, bool TWO = false, int LBW = 1, bool MATCH = false>
+// true when shared atomics return lane-ordered old values on this device
+// (checked once per device: 256 CTAs x 8 warps x 4 moduli x 512 rows)
+bool atoms_rank_ok() {
+  static int cached[64];
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  std::call_once(once[dev], [&] {
+    unsigned int* bad = nullptr;
+    unsigned int h = 1;
+    if (cudaMalloc(&bad, 4) == cudaSuccess && cudaMemset(bad, 0, 4) == cudaSuccess) {
+      atoms_order_check<<<256, 256>>>(bad, 512);
+      if (cudaMemcpy(&h, bad, 4, cudaMemcpyDeviceToHost) != cudaSuccess) h = 1;
+    }
+    if (bad) cudaFree(bad);
+    cudaGetLastError();
+    cached[dev] = h == 0 ? 1 : 2;
+  });
+  return cached[dev] == 1;
+}
+
+template <typename K, int I, int T, int LBW, int MINB>
+int launch_rf(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  const size_t smem = (size_t)T * I * sizeof(K) + (a.vin ? (size_t)T * I * 4 : 0);
+  if (a.vin) {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_rf_kernel<K, true, I, T, LBW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_rf_kernel<K, true, I, T, LBW, MINB><<<(unsigned)tiles, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
+  } else {
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_rf_kernel<K, false, I, T, LBW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_rf_kernel<K, false, I, T, LBW, MINB><<<(unsigned)tiles, T, smem, s>>>(
+        (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
+  }
+  return check_launch();
+}
+
+template <typename K, int I, int T = 512, bool TWO = false, int LBW = 1, bool MATCH = false, bool AR = false>
 int launch_ec(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
   const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
   *tiles_out = tiles;
   if (dry) return HB_OK;
   const size_t smem = (size_t)T * I * sizeof(K) + (a.vin ? (size_t)T * I * 4 : 0);
   if (a.vin) {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO, LBW, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, true, I, T, TWO, LBW, MATCH><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, true, I, T, TWO, LBW, MATCH, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, true, I, T, TWO, LBW, MATCH, AR><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   } else {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO, LBW, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_ec_kernel<K, false, I, T, TWO, LBW, MATCH><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_ec_kernel<K, false, I, T, TWO, LBW, MATCH, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_ec_kernel<K, false, I, T, TWO, LBW, MATCH, AR><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   }
   return check_launch();
@@ -977,7 +1164,10 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
       case 6: return launch_persist<K, 256, 8>(a, s, tiles, dry);
       case 8: return launch_tma<K, 256, 8>(a, s, tiles, dry);
       case 12: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
-      default: return launch_ec<K, 8>(a, s, tiles, dry);
+      case 13: return launch_ec<K, 8>(a, s, tiles, dry);
+      default:
+        if (atoms_rank_ok()) return launch_rf<K, 12, 256, 2, 3>(a, s, tiles, dry);
+        return launch_ec<K, 8>(a, s, tiles, dry);
     }
   } else {
   switch (sort_variant()) {
@@ -1008,9 +1198,29 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 12: return launch_pass<K, 256, 12, true>(a, s, tiles, dry);
     case 26: return launch_ec<K, 20, 384>(a, s, tiles, dry);
     case 27: return launch_ec<K, 20, 384, false, 2, true>(a, s, tiles, dry);
+    case 40: return launch_ec<K, 20, 384, false, 2, false, true>(a, s, tiles, dry);
+    case 41: return launch_ec<K, 24, 384, false, 2, false, true>(a, s, tiles, dry);
+    case 42: return launch_ec<K, 16, 384, false, 2, false, true>(a, s, tiles, dry);
+    case 43: return launch_ec<K, 16, 512, false, 2, false, true>(a, s, tiles, dry);
+    case 44: return launch_ec<K, 12, 512, false, 2, false, true>(a, s, tiles, dry);
+    case 50: return launch_rf<K, 20, 384, 2, 2>(a, s, tiles, dry);
+    case 51: return launch_rf<K, 12, 384, 2, 3>(a, s, tiles, dry);
+    case 52: return launch_rf<K, 16, 512, 2, 2>(a, s, tiles, dry);
+    case 53: return launch_rf<K, 24, 256, 2, 3>(a, s, tiles, dry);
+    case 54: return launch_rf<K, 16, 256, 2, 4>(a, s, tiles, dry);
+    case 55: return launch_rf<K, 14, 384, 2, 3>(a, s, tiles, dry);
+    case 56: return launch_rf<K, 28, 256, 2, 3>(a, s, tiles, dry);
+    case 57: return launch_rf<K, 20, 256, 2, 4>(a, s, tiles, dry);
+    case 58: return launch_rf<K, 24, 256, 4, 3>(a, s, tiles, dry);
+    case 59: return launch_rf<K, 32, 256, 2, 2>(a, s, tiles, dry);
+    case 60: return launch_rf<K, 22, 256, 2, 3>(a, s, tiles, dry);
+    case 61: return launch_rf<K, 24, 256, 1, 3>(a, s, tiles, dry);
     case 28: return launch_ec<K, 16, 384, false, 2, true>(a, s, tiles, dry);
     case 29: return launch_ec<K, 24, 384, false, 2, true>(a, s, tiles, dry);
-    default: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);  // best measured (round 1)
+    case 62: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);  // ballot ranking (42 Gkeys/s)
+    default:  // best measured (round 1): rank-first with lane-ordered shared atomics, 51 Gkeys/s
+      if (atoms_rank_ok()) return launch_rf<K, 22, 256, 2, 3>(a, s, tiles, dry);
+      return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);
   }
   }
 }

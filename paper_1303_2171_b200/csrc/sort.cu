@@ -110,6 +110,58 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+// uint32 keys: 16-byte loads (4 keys), 4 in flight per thread, and
+// LANE-STRIPED counters s[digit position][bucket][lane] (128 KB, one
+// 1024-thread CTA per SM): the four atomics of a key hit 32 distinct banks
+// across the warp for any data, like the 256-bin histogram kernel.
+constexpr int kDh32Threads = 1024;
+constexpr size_t kDh32Smem = (size_t)4 * 256 * 32 * 4;
+
+__global__ void __launch_bounds__(kDh32Threads, 1)
+    digit_hist32_kernel(const uint32_t* __restrict__ keys, int64_t n, uint32_t flip, uint32_t* __restrict__ hist) {
+  extern __shared__ __align__(16) uint32_t s32[];  // [4][256][32]
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += kDh32Threads) s32[i] = 0;
+  __syncthreads();
+  auto put = [&](uint32_t k) {
+    k ^= flip;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&s32[((p << 8) | ((k >> (8 * p)) & 255u)) * 32 + lane], 1u);
+  };
+  const int64_t nv = n >> 2;  // whole uint4 vectors (keys come from an aligned allocation)
+  const uint4* v = reinterpret_cast<const uint4*>(keys);
+  const int64_t stride = (int64_t)gridDim.x * kDh32Threads;
+  int64_t i = (int64_t)blockIdx.x * kDh32Threads + threadIdx.x;
+  constexpr int U = 4;
+  for (; i + (U - 1) * stride < nv; i += U * stride) {
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = ldg_stream_v4(v + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      put(q[u].x);
+      put(q[u].y);
+      put(q[u].z);
+      put(q[u].w);
+    }
+  }
+  for (; i < nv; i += stride) {
+    const uint4 q = ldg_stream_v4(v + i);
+    put(q.x);
+    put(q.y);
+    put(q.z);
+    put(q.w);
+  }
+  for (int64_t t = (nv << 2) + (int64_t)blockIdx.x * kDh32Threads + threadIdx.x; t < n; t += stride) put(keys[t]);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 4 * 256; b += kDh32Threads) {
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) sum += s32[b * 32 + ((l + b) & 31)];
+    if (sum) atomicAdd(hist + b, sum);
+  }
+}
+
 // ------------------------------------------------------------------ 2. onesweep pass
 // T threads x I items per tile; RANK_MATCH selects __match_any_sync (one
 // MATCH per key row) instead of the eight-ballot multi-split.
@@ -880,7 +932,7 @@ __global__ void __launch_bounds__(T, 1024 / T)
 // the ballot kernel is used if the check fails.  After the ranking pass the
 // counters hold the per-warp digit counts, so no separate counting pass is
 // needed; warps 0-7 then publish, scan and look back while the rest wait.
-template <typename K, bool HAS_V, int I, int T, int LBW, int MINB>
+template <typename K, bool HAS_V, int I, int T, int LBW, int MINB, bool ES = false>
 __global__ void __launch_bounds__(T, MINB)
     onesweep_rf_kernel(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                        uint32_t* __restrict__ vout, int64_t n, int shift, K flip,
@@ -921,9 +973,9 @@ __global__ void __launch_bounds__(T, MINB)
   for (int i = 0; i < I; ++i) rank[i] = atomicAdd(&s_base[warp][digit_of<K>(key[i], flip, shift)], 1u);
   __syncthreads();
 
+  const int d = tid;  // digit of the look-back thread (tid < 256)
+  uint32_t c = 0, dstart = 0;
   if (tid < 256) {
-    const int d = tid;
-    uint32_t c = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) c += s_base[w][d];
     if (tile == 0) st_relaxed(lookback + d, kFlagInc | c);
@@ -938,7 +990,7 @@ __global__ void __launch_bounds__(T, MINB)
     bar_named(1, 256);
     uint32_t add = 0;
     for (int g = 0; g < warp; ++g) add += s_scr[g];
-    const uint32_t dstart = x - c + add;
+    dstart = x - c + add;
     uint32_t run = dstart;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -946,6 +998,22 @@ __global__ void __launch_bounds__(T, MINB)
       s_base[w][d] = run;
       run += t;
     }
+  }
+  auto scatter_smem = [&]() {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const uint32_t p = s_base[warp][digit_of<K>(key[i], flip, shift)] + rank[i];
+      s_keys[p] = key[i];
+      if (HAS_V) s_vals[p] = val[i];
+    }
+  };
+  if (ES) {
+    // local re-order first: the predecessors' aggregates land meanwhile, so
+    // the look-back below spins less
+    __syncthreads();
+    scatter_smem();
+  }
+  if (tid < 256) {
     uint32_t excl = 0;
     if (tile > 0) {
       int64_t t = (int64_t)tile - 1;
@@ -974,13 +1042,10 @@ __global__ void __launch_bounds__(T, MINB)
     s_goff[d] = gs + excl - dstart;
   }
   __syncthreads();
-#pragma unroll
-  for (int i = 0; i < I; ++i) {
-    const uint32_t p = s_base[warp][digit_of<K>(key[i], flip, shift)] + rank[i];
-    s_keys[p] = key[i];
-    if (HAS_V) s_vals[p] = val[i];
+  if (!ES) {
+    scatter_smem();
+    __syncthreads();
   }
-  __syncthreads();
   for (int j = tid; j < valid; j += T) {
     const K k = s_keys[j];
     const uint32_t dst = s_goff[digit_of<K>(k, flip, shift)] + (uint32_t)j;
@@ -1043,19 +1108,19 @@ bool atoms_rank_ok() {
   return cached[dev] == 1;
 }
 
-template <typename K, int I, int T, int LBW, int MINB>
+template <typename K, int I, int T, int LBW, int MINB, bool ES = false>
 int launch_rf(const PassArgs& a, cudaStream_t s, int64_t* tiles_out, bool dry) {
   const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
   *tiles_out = tiles;
   if (dry) return HB_OK;
   const size_t smem = (size_t)T * I * sizeof(K) + (a.vin ? (size_t)T * I * 4 : 0);
   if (a.vin) {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_rf_kernel<K, true, I, T, LBW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_rf_kernel<K, true, I, T, LBW, MINB><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_rf_kernel<K, true, I, T, LBW, MINB, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_rf_kernel<K, true, I, T, LBW, MINB, ES><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   } else {
-    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_rf_kernel<K, false, I, T, LBW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    onesweep_rf_kernel<K, false, I, T, LBW, MINB><<<(unsigned)tiles, T, smem, s>>>(
+    HB_CUDA_TRY(cudaFuncSetAttribute(onesweep_rf_kernel<K, false, I, T, LBW, MINB, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    onesweep_rf_kernel<K, false, I, T, LBW, MINB, ES><<<(unsigned)tiles, T, smem, s>>>(
         (const K*)a.kin, (K*)a.kout, nullptr, nullptr, a.n, a.shift, (K)a.flip, a.gstart, a.lookback, a.counter);
   }
   return check_launch();
@@ -1166,7 +1231,7 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
       case 12: return launch_pass<K, 256, 8, true>(a, s, tiles, dry);
       case 13: return launch_ec<K, 8>(a, s, tiles, dry);
       default:
-        if (atoms_rank_ok()) return launch_rf<K, 12, 256, 2, 3>(a, s, tiles, dry);
+        if (atoms_rank_ok()) return launch_rf<K, 12, 256, 2, 3, true>(a, s, tiles, dry);
         return launch_ec<K, 8>(a, s, tiles, dry);
     }
   } else {
@@ -1215,11 +1280,15 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
     case 59: return launch_rf<K, 32, 256, 2, 2>(a, s, tiles, dry);
     case 60: return launch_rf<K, 22, 256, 2, 3>(a, s, tiles, dry);
     case 61: return launch_rf<K, 24, 256, 1, 3>(a, s, tiles, dry);
+    case 63: return launch_rf<K, 22, 256, 2, 3, true>(a, s, tiles, dry);
+    case 64: return launch_rf<K, 24, 256, 2, 3, true>(a, s, tiles, dry);
+    case 65: return launch_rf<K, 20, 384, 2, 2, true>(a, s, tiles, dry);
+    case 66: return launch_rf<K, 22, 256, 4, 3, true>(a, s, tiles, dry);
     case 28: return launch_ec<K, 16, 384, false, 2, true>(a, s, tiles, dry);
     case 29: return launch_ec<K, 24, 384, false, 2, true>(a, s, tiles, dry);
     case 62: return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);  // ballot ranking (42 Gkeys/s)
-    default:  // best measured (round 1): rank-first with lane-ordered shared atomics, 51 Gkeys/s
-      if (atoms_rank_ok()) return launch_rf<K, 22, 256, 2, 3>(a, s, tiles, dry);
+    default:  // best measured (round 1): rank-first with lane-ordered shared atomics + early re-order, 52 Gkeys/s
+      if (atoms_rank_ok()) return launch_rf<K, 24, 256, 2, 3, true>(a, s, tiles, dry);
       return launch_ec<K, 20, 384, false, 2>(a, s, tiles, dry);
   }
   }
@@ -1241,7 +1310,19 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
   HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, (size_t)P * 256 * 4, s));
   int64_t hb = ceil_div(n, 512 * 8);
   if (hb > (int64_t)di.sms * 2) hb = (int64_t)di.sms * 2;
-  digit_hist_kernel<K><<<(int)hb, 512, 0, s>>>(keys, n, flip, hist.as<uint32_t>());
+  if constexpr (sizeof(K) == 4) {
+    if (((uintptr_t)keys & 15) == 0 && sort_variant() != 62) {
+      HB_CUDA_TRY(cudaFuncSetAttribute(digit_hist32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDh32Smem));
+      DeviceInfo di;
+      HB_TRY(device_info(&di));
+      digit_hist32_kernel<<<di.sms, kDh32Threads, kDh32Smem, s>>>(reinterpret_cast<const uint32_t*>(keys), n,
+                                                                   (uint32_t)flip, hist.as<uint32_t>());
+    } else {
+      digit_hist_kernel<K><<<(int)hb, 512, 0, s>>>(keys, n, flip, hist.as<uint32_t>());
+    }
+  } else {
+    digit_hist_kernel<K><<<(int)hb, 512, 0, s>>>(keys, n, flip, hist.as<uint32_t>());
+  }
   HB_TRY(check_launch());
   uint32_t h[P * 256];
   HB_CUDA_TRY(cudaMemcpyAsync(h, hist.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -572,7 +572,7 @@ class SortBench:
 
     name = "sort"
     unit = "Mkeys/s"
-    kernel = "onesweep_rf_kernel"
+    kernel = "onesweep_rfk_kernel"
 
     def __init__(self, n: int = 1 << 28, seed: int = 42):
         self.n, self.seed = n, seed

@@ -1054,6 +1054,133 @@ __global__ void __launch_bounds__(T, MINB)
   }
 }
 
+// u32 keys + u32 payload moved as ONE 8-byte element (key in the low half):
+// PIN — the input is packed (else key and payload arrays), POUT — the output
+// is packed (else split back into the two arrays).  The first live digit pass
+// reads split and writes packed, the middle passes stay packed, the last one
+// writes split: one 8-byte load / smem store / smem load / global store per
+// element instead of two of each.
+template <bool PIN, bool POUT, int I, int T, int LBW, int MINB>
+__global__ void __launch_bounds__(T, MINB)
+    onesweep_rfk_kernel(const void* __restrict__ kin_, void* __restrict__ kout_, const uint32_t* __restrict__ vin,
+                        uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t flip,
+                       const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
+                       uint32_t* __restrict__ tile_counter) {
+  constexpr int W = T / 32, TILE = T * I;
+  static_assert(T >= 256, "one look-back thread per digit");
+  __shared__ uint32_t s_base[W][256];  // per-warp running counts → per-(warp, digit) tile positions
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_scr[8];
+  __shared__ uint32_t s_tile;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  uint64_t* s_el = reinterpret_cast<uint64_t*>(s_dyn);
+  const uint32_t* kin = reinterpret_cast<const uint32_t*>(kin_);
+  const uint64_t* ein = reinterpret_cast<const uint64_t*>(kin_);
+  uint32_t* kout = reinterpret_cast<uint32_t*>(kout_);
+  uint64_t* eout = reinterpret_cast<uint64_t*>(kout_);
+  auto dig = [&](uint64_t e) -> uint32_t { return (((uint32_t)e ^ flip) >> shift) & 255u; };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < W * 256; i += T) (&s_base[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * TILE;
+  const int valid = (int)min((int64_t)TILE, n - base);
+  const int wbase = warp * 32 * I;
+  uint64_t el[I];
+  uint32_t rank[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+    const int idx = wbase + i * 32 + lane;
+    const bool ok = idx < valid;
+    if (PIN) el[i] = ok ? ein[base + idx] : (uint64_t)(~0u ^ flip);
+    else el[i] = ok ? ((uint64_t)vin[base + idx] << 32) | kin[base + idx] : (uint64_t)(~0u ^ flip);
+  }
+  uint32_t gs = 0;
+  if (tid < 256) gs = gstart[tid];
+#pragma unroll
+  for (int i = 0; i < I; ++i) rank[i] = atomicAdd(&s_base[warp][dig(el[i])], 1u);
+  __syncthreads();
+
+  const int d = tid;  // digit of the look-back thread (tid < 256)
+  uint32_t c = 0, dstart = 0;
+  if (tid < 256) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) c += s_base[w][d];
+    if (tile == 0) st_relaxed(lookback + d, kFlagInc | c);
+    else st_relaxed(lookback + (size_t)tile * 256 + d, kFlagAgg | c);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_scr[warp] = x;
+    bar_named(1, 256);
+    uint32_t add = 0;
+    for (int g = 0; g < warp; ++g) add += s_scr[g];
+    dstart = x - c + add;
+    uint32_t run = dstart;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t t = s_base[w][d];
+      s_base[w][d] = run;
+      run += t;
+    }
+  }
+  auto scatter_smem = [&]() {
+#pragma unroll
+    for (int i = 0; i < I; ++i) s_el[s_base[warp][dig(el[i])] + rank[i]] = el[i];
+  };
+  {  // local re-order before the look-back walk (see onesweep_rf_kernel)
+    // local re-order first: the predecessors' aggregates land meanwhile, so
+    // the look-back below spins less
+    __syncthreads();
+    scatter_smem();
+  }
+  if (tid < 256) {
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      bool done = false;
+      while (!done) {
+        uint32_t wv[LBW];
+#pragma unroll
+        for (int j = 0; j < LBW; ++j) {
+          const int64_t tj = t - j < 0 ? 0 : t - j;
+          wv[j] = ld_relaxed(lookback + (size_t)tj * 256 + d);
+        }
+        int used = 0;
+#pragma unroll
+        for (int j = 0; j < LBW; ++j) {
+          if (done || used < j) continue;
+          const uint32_t flag = wv[j] & ~kCountMask;
+          if (flag == 0) continue;
+          excl += wv[j] & kCountMask;
+          used = j + 1;
+          if (flag == kFlagInc) done = true;
+        }
+        t -= used;
+      }
+      st_relaxed(lookback + (size_t)tile * 256 + d, kFlagInc | (excl + c));
+    }
+    s_goff[d] = gs + excl - dstart;
+  }
+  __syncthreads();
+  for (int j = tid; j < valid; j += T) {
+    const uint64_t e = s_el[j];
+    const uint32_t dst = s_goff[dig(e)] + (uint32_t)j;
+    if (POUT) {
+      eout[dst] = e;
+    } else {
+      kout[dst] = (uint32_t)e;
+      vout[dst] = (uint32_t)(e >> 32);
+    }
+  }
+}
+
+
 // device check of the lane-ordered shared atomics the rank-first kernel relies on
 __global__ void atoms_order_check(unsigned int* bad, int rows) {
   __shared__ uint32_t cnt[8][256];
@@ -1106,6 +1233,27 @@ bool atoms_rank_ok() {
     cached[dev] = h == 0 ? 1 : 2;
   });
   return cached[dev] == 1;
+}
+
+template <bool PIN, bool POUT, int I, int T, int LBW, int MINB>
+int launch_rfk_impl(const PassArgs& a, cudaStream_t s, int64_t tiles) {
+  const size_t smem = (size_t)T * I * 8;
+  auto k = onesweep_rfk_kernel<PIN, POUT, I, T, LBW, MINB>;
+  HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)tiles, T, smem, s>>>(a.kin, a.kout, a.vin, a.vout, a.n, a.shift, (uint32_t)a.flip, a.gstart, a.lookback,
+                                     a.counter);
+  return check_launch();
+}
+
+template <int I, int T, int LBW, int MINB>
+int launch_rfk(const PassArgs& a, bool pin, bool pout, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  if (pin && pout) return launch_rfk_impl<true, true, I, T, LBW, MINB>(a, s, tiles);
+  if (pin) return launch_rfk_impl<true, false, I, T, LBW, MINB>(a, s, tiles);
+  if (pout) return launch_rfk_impl<false, true, I, T, LBW, MINB>(a, s, tiles);
+  return launch_rfk_impl<false, false, I, T, LBW, MINB>(a, s, tiles);
 }
 
 template <typename K, int I, int T, int LBW, int MINB, bool ES = false>
@@ -1294,6 +1442,42 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
   }
 }
 
+// live digit passes of a u32-key + u32-payload sort with the pair moved as one
+// 8-byte element: split → packed → … → packed → split (back into keys/vals)
+template <int PI, int PT, int LBW, int MINB>
+int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, const bool* live, int nlive,
+                  const DevBuf& hist, const DevBuf& gst, DevBuf& lb, cudaStream_t s) {
+  int64_t tiles = 0;
+  PassArgs pa{};
+  pa.n = n;
+  HB_TRY((launch_rfk<PI, PT, LBW, MINB>(pa, false, false, s, &tiles, true)));
+  const size_t lb_words = (size_t)tiles * 256 + 32;
+  DevBuf pA, pB;
+  HB_TRY(alloc(&lb, lb_words * 4, s));
+  HB_TRY(alloc(&pA, (size_t)n * 8, s));
+  if (nlive >= 3) HB_TRY(alloc(&pB, (size_t)n * 8, s));
+  uint32_t* counter = lb.as<uint32_t>() + (size_t)tiles * 256;
+  void* cur = keys;
+  void* nxt = pA.ptr;
+  int done = 0;
+  for (int p = 0; p < 4; ++p) {
+    if (!live[p]) continue;
+    const bool first = done == 0, last = done == nlive - 1;
+    HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
+    pa.kin = cur;
+    pa.kout = last ? (void*)keys : nxt;
+    pa.vin = first ? vals : nullptr;
+    pa.vout = last ? vals : nullptr;
+    pa.shift = 8 * p; pa.flip = (uint64_t)flip; pa.hist = hist.as<uint32_t>() + p * 256;
+    pa.lookback = lb.as<uint32_t>(); pa.counter = counter; pa.gstart = gst.as<uint32_t>() + p * 256;
+    HB_TRY((launch_rfk<PI, PT, LBW, MINB>(pa, !first, !last, s, &tiles, false)));
+    cur = nxt;
+    nxt = (nxt == pA.ptr) ? pB.ptr : pA.ptr;
+    ++done;
+  }
+  return HB_OK;
+}
+
 template <typename K>
 int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cudaStream_t s) {
   constexpr int P = SortCfg<K>::kPasses;
@@ -1342,11 +1526,24 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
   HB_TRY(alloc(&gst, (size_t)P * 256 * 4, s));
   scan_hist_kernel<<<P, 256, 0, s>>>(hist.as<uint32_t>(), gst.as<uint32_t>(), P);
   HB_TRY(check_launch());
-  HB_TRY(alloc(&kalt, (size_t)n * sizeof(K), s));
-  if (vals) HB_TRY(alloc(&valt, (size_t)n * 4, s));
   int64_t tiles = 0;
   PassArgs pa{};
   pa.n = n;
+  if constexpr (sizeof(K) == 4) {
+    // key + payload as one 8-byte element between the first and the last live pass
+    const int v = sort_variant();
+    if (vals && nlive >= 2 && (v == 0 || (v >= 74 && v <= 77)) && atoms_rank_ok()) {
+      switch (v) {
+        case 75: return packed_passes<20, 256, 2, 3>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
+        case 76: return packed_passes<24, 256, 2, 3>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
+        case 77: return packed_passes<16, 256, 2, 4>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
+        default:  // best measured: 22 keys/thread, 59.5 Gkeys/s (24: 57.4, 20: 55.6)
+          return packed_passes<22, 256, 2, 3>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
+      }
+    }
+  }
+  HB_TRY(alloc(&kalt, (size_t)n * sizeof(K), s));
+  if (vals) HB_TRY(alloc(&valt, (size_t)n * 4, s));
   HB_TRY(run_pass<K>(pa, s, &tiles, true));
   const size_t lb_words = (size_t)tiles * 256 + 32;  // + tile counter (padded)
   HB_TRY(alloc(&lb, lb_words * 4, s));

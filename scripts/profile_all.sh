@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu --set full capture of each workload's dominant kernel + the launch list of one bench step.
 mkdir -p gpurun_out/prof
-for spec in "hist:hist_striped" "spmv:spmv_lpr" "sort:onesweep_rf" "bilat:bilateral_tma" "conv:conv_rows" "lr:lr_walk_kernel"; do
+for spec in "hist:hist_striped" "spmv:spmv_lpr" "sort:onesweep_rfk" "bilat:bilateral_tma" "conv:conv_rows" "lr:lr_walk_kernel"; do
   w=${spec%%:*}; k=${spec##*:}
   ncu --set full --import-source on --clock-control none -k regex:$k -s 1 -c 1 -o gpurun_out/prof/$w -f \
       python bench.py --workload $w --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/prof/$w.log 2>&1

@@ -282,6 +282,17 @@ __global__ void __launch_bounds__(kThreads, MINB)
       num[k][j] = den[k][j] = 0.0;
     }
   const double* lane_rng = rng + lane + (SYM ? 255 * 16 : 0);
+  // SYM: per-pixel shared-memory byte address of range[nb - c] is
+  // cbase[j] + nb*128 (the table row of difference 0, minus c rows), so a tap
+  // costs one 32-bit add + one LDS instead of subtract + multiply-add
+  uint32_t cbase[NR][kPx];
+  if (SYM) {
+    const uint32_t lr = (uint32_t)__cvta_generic_to_shared(lane_rng);
+#pragma unroll
+    for (int k = 0; k < NR; ++k)
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) cbase[k][j] = lr - (uint32_t)c[k][j] * 128u;
+  }
 #pragma unroll 1
   for (int iy = 0; iy < S + NR - 1; ++iy) {
     int nb[kPx + 2 * R];
@@ -291,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (int q = 0; q < kPx + 2 * R; ++q) {
       nb[q] = trow[q];
       nbd[q] = (double)nb[q];
+      if (SYM) nb[q] *= 128;  // byte offset of the intensity's table row
     }
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -301,8 +313,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const double s = sp[dy * S + dx];
 #pragma unroll
         for (int j = 0; j < kPx; ++j) {
-          const int d = SYM ? nb[j + dx] - c[k][j] : abs(nb[j + dx] - c[k][j]);
-          const double w = __dmul_rn(s, lane_rng[d * 16]);
+          double r;
+          if (SYM) {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(cbase[k][j] + (uint32_t)nb[j + dx]));
+          } else {
+            r = lane_rng[abs(nb[j + dx] - c[k][j]) * 16];
+          }
+          const double w = __dmul_rn(s, r);
           num[k][j] = __dadd_rn(num[k][j], __dmul_rn(w, nbd[j + dx]));
           den[k][j] = __dadd_rn(den[k][j], w);
         }

@@ -495,8 +495,6 @@ extern "C" int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width
     in1 = row1 + radius > height ? height : row1 + radius;
   }
   DevBuf d_img, d_sp, d_rg, d_out;
-  const uint8_t* src = dev ? img : img + (int64_t)in0 * width;
-  HB_TRY(stage_in(&d_img, src, (size_t)(in1 - in0) * width, dev, s));
   HB_TRY(stage_in(&d_sp, spatial, (size_t)S * S * 8, dev, s));
   HB_TRY(stage_in(&d_rg, range256, 256 * 8, dev, s));
   const size_t es = out_code == 64 ? 8 : 4;
@@ -504,11 +502,21 @@ extern "C" int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width
   HB_TRY(stage_out(&d_out, out, out_bytes, dev, s));
   // the kernel sees a (in1-in0)-row image; clamping at its edges equals
   // clamping at the true image edges because the staged rows cover the halo
-  const int h = in1 - in0, r0 = row0 - in0, r1 = row1 - in0;
-  int rc = out_code == 64
-               ? launch_bilateral<double>(d_img.as<uint8_t>(), h, width, r0, r1, radius, d_sp.as<double>(), d_rg.as<double>(), d_out.as<double>(), s)
-               : launch_bilateral<float>(d_img.as<uint8_t>(), h, width, r0, r1, radius, d_sp.as<double>(), d_rg.as<double>(), d_out.as<float>(), s);
-  if (rc != HB_OK) return rc;
-  HB_TRY(copy_out(out, d_out, out_bytes, dev, s));
+  const int h = in1 - in0;
+  auto launch = [&](int a, int b) -> int {  // absolute rows [a, b)
+    char* o = d_out.as<char>() + (size_t)(a - row0) * width * es;
+    return out_code == 64
+               ? launch_bilateral<double>(d_img.as<uint8_t>(), h, width, a - in0, b - in0, radius, d_sp.as<double>(), d_rg.as<double>(), reinterpret_cast<double*>(o), s)
+               : launch_bilateral<float>(d_img.as<uint8_t>(), h, width, a - in0, b - in0, radius, d_sp.as<double>(), d_rg.as<double>(), reinterpret_cast<float*>(o), s);
+  };
+  if (dev) {
+    d_img.ptr = const_cast<uint8_t*>(img);
+    HB_TRY(launch(row0, row1));
+  } else {
+    // host buffers: row chunks with H2D / kernel / D2H overlapped
+    HB_TRY(alloc(&d_img, (size_t)h * width, s));
+    HB_TRY(row_pipeline(reinterpret_cast<const char*>(img) + (size_t)in0 * width, width, in0, in1, radius, row0,
+                        row1, reinterpret_cast<char*>(out), width * es, d_img.as<char>(), d_out.as<char>(), s, launch));
+  }
   return finish(flags, s);
 }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <functional>
 #include <string>
 
 #include "../../include/hb200.h"
@@ -78,6 +79,12 @@ int copy_out(void* dst, const DevBuf& b, size_t bytes, bool device, cudaStream_t
 int copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int finish(int flags, cudaStream_t s);  // sync unless HB_ASYNC, surface errors
+// Host-buffer row filters: H2D of input rows (on a side stream), the kernel
+// of each row chunk on `s` (launch(a, b) = absolute rows [a, b)), D2H of the
+// chunk's output rows on another side stream; returns with the output landed.
+int row_pipeline(const char* in_host, size_t in_row, int in0, int in1, int radius, int row0, int row1,
+                 char* out_host, size_t out_row, char* d_in, char* d_out, cudaStream_t s,
+                 const std::function<int(int, int)>& launch);
 int check_launch();
 
 // ------------------------------------------------------------------ PTX helpers

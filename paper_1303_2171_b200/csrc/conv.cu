@@ -361,10 +361,9 @@ extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t
     in1 = row1 + radius > height ? height : row1 + radius;
   }
   DevBuf d_img, d_w, d_out;
-  const char* src = reinterpret_cast<const char*>(img) + (dev ? 0 : (size_t)in0 * width * es_in);
-  HB_TRY(stage_in(&d_img, src, (size_t)(in1 - in0) * width * es_in, dev, s));
   HB_TRY(stage_in(&d_w, weights, (size_t)S * S * 8, dev, s));
-  const size_t out_bytes = (size_t)(row1 - row0) * width * (out_code == 64 ? 8 : 4);
+  const size_t es_out = out_code == 64 ? 8 : 4;
+  const size_t out_bytes = (size_t)(row1 - row0) * width * es_out;
   HB_TRY(stage_out(&d_out, out, out_bytes, dev, s));
   // no zero tap → the branch-free kernel (the zero-skip test is the only
   // data-dependent branch of the tap loop); weights are read on the host
@@ -379,11 +378,22 @@ extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t
     }
     for (double v : hw) dense &= v != 0.0;
   }
-  const int h = in1 - in0, r0 = row0 - in0, r1 = row1 - in0;
-  const int rc = in_code == HB_U8
-                     ? dispatch_out<uint8_t>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), dense, d_out.ptr, out_code, s)
-                     : dispatch_out<double>(d_img.ptr, h, width, r0, r1, radius, d_w.as<double>(), dense, d_out.ptr, out_code, s);
-  if (rc != HB_OK) return rc;
-  HB_TRY(copy_out(out, d_out, out_bytes, dev, s));
+  const int h = in1 - in0;
+  auto launch = [&](int a, int b) -> int {  // absolute rows [a, b)
+    void* o = d_out.as<char>() + (size_t)(a - row0) * width * es_out;
+    return in_code == HB_U8
+               ? dispatch_out<uint8_t>(d_img.ptr, h, width, a - in0, b - in0, radius, d_w.as<double>(), dense, o, out_code, s)
+               : dispatch_out<double>(d_img.ptr, h, width, a - in0, b - in0, radius, d_w.as<double>(), dense, o, out_code, s);
+  };
+  if (dev) {
+    d_img.ptr = const_cast<void*>(img);
+    HB_TRY(launch(row0, row1));
+  } else {
+    // host buffers: row chunks with H2D / kernel / D2H overlapped
+    HB_TRY(alloc(&d_img, (size_t)h * width * es_in, s));
+    HB_TRY(row_pipeline(reinterpret_cast<const char*>(img) + (size_t)in0 * width * es_in, width * es_in, in0, in1,
+                        radius, row0, row1, reinterpret_cast<char*>(out), width * es_out, d_img.as<char>(),
+                        d_out.as<char>(), s, launch));
+  }
   return finish(flags, s);
 }

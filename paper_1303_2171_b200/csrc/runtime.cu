@@ -289,6 +289,76 @@ int copy_out(void* dst, const DevBuf& b, size_t bytes, bool device, cudaStream_t
   return copy_d2h(dst, b.ptr, bytes, s);
 }
 
+// Row-strip pipeline for host-buffer filter calls.  Three streams: input
+// rows cross PCIe on `is`, the kernel of chunk c runs on `s` once its rows
+// (and halo) have landed, and chunk c's output rows go back on `cs` as soon
+// as its kernel is done — so the D2H of chunk c overlaps the kernel of chunk
+// c+1, and H2D runs beside D2H (PCIe is full duplex).  Always drains both
+// side streams before returning, so the caller's stream-ordered buffers
+// (freed on `s`) are not released under a copy in flight.
+int row_pipeline(const char* in_host, size_t in_row, int in0, int in1, int radius, int row0, int row1,
+                 char* out_host, size_t out_row, char* d_in, char* d_out, cudaStream_t s,
+                 const std::function<int(int, int)>& launch) {
+  const int rows = row1 - row0;
+  if (rows <= 0) return HB_OK;
+  const size_t out_bytes = (size_t)rows * out_row;
+  const int chunks = (int)std::min<size_t>({(size_t)16, (size_t)rows, std::max<size_t>(1, out_bytes >> 26)});
+  const int per = (rows + chunks - 1) / chunks;
+  if (chunks == 1) {  // small strips: in, kernel, out on `s`
+    HB_TRY(copy_h2d(d_in, in_host, (size_t)(in1 - in0) * in_row, s));
+    HB_TRY(launch(row0, row1));
+    return copy_d2h(out_host, d_out, out_bytes, s);
+  }
+  struct Side {
+    cudaStream_t is = nullptr, cs = nullptr;
+    std::vector<cudaEvent_t> in_ev, k_ev;
+    ~Side() {
+      if (is) cudaStreamSynchronize(is);
+      if (cs) cudaStreamSynchronize(cs);
+      for (cudaEvent_t e : in_ev) if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : k_ev) if (e) cudaEventDestroy(e);
+      if (is) cudaStreamDestroy(is);
+      if (cs) cudaStreamDestroy(cs);
+    }
+  } side;
+  HB_CUDA_TRY(cudaStreamCreateWithFlags(&side.is, cudaStreamNonBlocking));
+  HB_CUDA_TRY(cudaStreamCreateWithFlags(&side.cs, cudaStreamNonBlocking));
+  side.in_ev.assign(chunks, nullptr);
+  side.k_ev.assign(chunks, nullptr);
+  for (int c = 0; c < chunks; ++c) {
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&side.in_ev[c], cudaEventDisableTiming));
+    HB_CUDA_TRY(cudaEventCreateWithFlags(&side.k_ev[c], cudaEventDisableTiming));
+  }
+  // the device buffers were allocated on `s`: the side streams start after that
+  HB_CUDA_TRY(cudaEventRecord(side.k_ev[0], s));
+  HB_CUDA_TRY(cudaStreamWaitEvent(side.is, side.k_ev[0], 0));
+  HB_CUDA_TRY(cudaStreamWaitEvent(side.cs, side.k_ev[0], 0));
+  // chunk c's kernel needs input rows [in0, need_c) resident
+  int loaded = in0;
+  for (int c = 0; c < chunks; ++c) {
+    const int a = row0 + c * per, b = std::min(row1, a + per);
+    const int need = c + 1 == chunks ? in1 : std::min(in1, b + radius);
+    if (need > loaded) {
+      HB_TRY(copy_h2d(d_in + (size_t)(loaded - in0) * in_row, in_host + (size_t)(loaded - in0) * in_row,
+                      (size_t)(need - loaded) * in_row, side.is));
+      loaded = need;
+    }
+    HB_CUDA_TRY(cudaEventRecord(side.in_ev[c], side.is));
+    HB_CUDA_TRY(cudaStreamWaitEvent(s, side.in_ev[c], 0));
+    if (a < b) HB_TRY(launch(a, b));
+    HB_CUDA_TRY(cudaEventRecord(side.k_ev[c], s));
+  }
+  for (int c = 0; c < chunks; ++c) {
+    const int a = row0 + c * per, b = std::min(row1, a + per);
+    if (a >= b) continue;
+    HB_CUDA_TRY(cudaStreamWaitEvent(side.cs, side.k_ev[c], 0));
+    HB_TRY(copy_d2h(out_host + (size_t)(a - row0) * out_row, d_out + (size_t)(a - row0) * out_row,
+                    (size_t)(b - a) * out_row, side.cs));
+  }
+  HB_CUDA_TRY(cudaStreamSynchronize(side.cs));
+  return check_launch();
+}
+
 int check_launch() {
   HB_CUDA_TRY(cudaGetLastError());
   return HB_OK;

@@ -106,6 +106,30 @@ def out_like(device: bool, shape: Any, dtype: Any, ref: Any = None) -> Any:
     return np.empty(shape, dtype=dtype)
 
 
+PINNED_MIN_BYTES = 4 << 20
+PINNED_MAX_BYTES = 8 << 30
+
+
+def host_empty(shape: Any, dtype: Any = np.float64) -> np.ndarray:
+    """An uninitialised host array for a result the GPU writes back.  Large
+    results come from torch's caching pinned-host allocator (a numpy view
+    that keeps its block alive; the block returns to the cache when the
+    array is dropped), so the D2H is one DMA straight into the result — no
+    pageable staging pass, no first-touch page faults on a fresh multi-GB
+    np.empty.  Small results, results above PINNED_MAX_BYTES and hosts
+    without CUDA get a plain np.empty."""
+    dt = np.dtype(dtype)
+    shape = (int(shape),) if np.ndim(shape) == 0 else tuple(int(d) for d in shape)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
+    if (torch is not None and PINNED_MIN_BYTES <= nbytes <= PINNED_MAX_BYTES and dt in _TORCH_TO_NP.values()
+            and torch.cuda.is_available()):
+        try:
+            return torch.empty(shape, dtype=_np_to_torch(dt), pin_memory=True).numpy()
+        except RuntimeError:  # pinned memory exhausted: pageable result
+            pass
+    return np.empty(shape, dtype=dt)
+
+
 def _np_to_torch(dt: np.dtype):
     for k, v in _TORCH_TO_NP.items():
         if v == dt:

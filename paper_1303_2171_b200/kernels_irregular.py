@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib, sharding
 from .errors import DataIOError, StructuralError
-from .gpu import buf, current_stream_handle, is_device_array, require_gpu, to_host, vp
+from .gpu import buf, current_stream_handle, host_empty, is_device_array, require_gpu, to_host, vp
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
 
@@ -504,7 +504,7 @@ def gpu_list_rank(succ: Any, head: int, out: Any = None, *, asynchronous: bool =
         _lib.call("hb_list_rank", vp(sb.ptr), code, n, int(head), vp(res.data_ptr()), flags,
                   current_stream_handle(succ))
         return res
-    res = np.empty(n, dtype=np.int64)
+    res = host_empty(n, np.int64)
     _lib.call("hb_list_rank", vp(sb.ptr), code, n, int(head), vp(res.ctypes.data), 0, current_stream_handle())
     return res
 

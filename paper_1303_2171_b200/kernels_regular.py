@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib, sharding
 from .errors import DataIOError
-from .gpu import buf, current_stream_handle, flags_for, is_device_array, require_gpu, to_host, vp
+from .gpu import buf, current_stream_handle, flags_for, host_empty, is_device_array, require_gpu, to_host, vp
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
 
@@ -256,8 +256,8 @@ def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False) -> t
         k_out, v_out = kb.ptr, (vb.ptr if vb else 0)
         res_k, res_v = keys, payload
     else:
-        res_k = np.empty_like(kb.owner)
-        res_v = np.empty(kb.size, dtype=vb.dtype) if vb else None
+        res_k = host_empty(kb.owner.shape, kb.dtype)
+        res_v = host_empty(kb.size, vb.dtype) if vb else None
         k_out, v_out = res_k.ctypes.data, (res_v.ctypes.data if vb else 0)
     passes = ctypes.c_int32(0)
     _lib.call("hb_sort", vp(kb.ptr), vp(k_out), code, vp(vb.ptr if vb else 0), vp(v_out), kb.size,
@@ -389,15 +389,15 @@ def _host_rows_out(out: np.ndarray | None, rows: int, width: int) -> np.ndarray:
 
 class _StripOutput:
     """Both sides of a host-image run write their row strips straight into one
-    output image allocated by partition() (np.empty: no page is touched until
-    a side writes its strip), so merge() hands that image back instead of the
+    output image allocated by partition() (host_empty: pinned, so the GPU
+    strip lands by DMA), so merge() hands that image back instead of the
     reference's vstack copy (an extra pass over H×W×8 bytes).  Device images
     and GPU groups keep the partial-array protocol."""
 
     def _new_output(self, height: int, width: int) -> None:
         pix = self.image.pixels
         local = not is_device_array(pix) and (sharding.active_group() is None or sharding.active_group().world == 1)
-        self._out = np.empty((height, width)) if local else None
+        self._out = host_empty((height, width)) if local else None
 
     def _strip(self, part) -> np.ndarray | None:
         out = getattr(self, "_out", None)
@@ -505,7 +505,7 @@ def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, o
         arr = arr.astype(np.float64)
     img = buf(arr)
     if out is None:
-        out = np.empty((row1 - row0, width), dtype=np.float64 if code == 64 else np.float32)
+        out = host_empty((row1 - row0, width), np.float64 if code == 64 else np.float32)
     if row1 == row0:
         return out
     _lib.call("hb_convolve", vp(img.ptr), img.code, height, width, kernel.radius, vp(w.ctypes.data),
@@ -645,7 +645,7 @@ def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out
         return out
     img = buf(pixels, np.uint8)
     if out is None:
-        out = np.empty((row1 - row0, width), dtype=np.float64 if code == 64 else np.float32)
+        out = host_empty((row1 - row0, width), np.float64 if code == 64 else np.float32)
     if row1 == row0:
         return out
     sp = np.ascontiguousarray(lut.spatial_weights, dtype=np.float64)

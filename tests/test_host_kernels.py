@@ -138,3 +138,14 @@ def test_measured_calibration_finds_the_balanced_split():
     assert share.origin is ShareOrigin.CALIBRATED
     assert abs(share.fraction_a - 1 / 3) < 0.06, share.fraction_a
     assert share.probe.t_device_a > share.probe.t_device_b
+
+
+def test_host_empty_shapes_and_dtypes():
+    import numpy as np
+
+    from paper_1303_2171_b200.gpu import host_empty
+
+    for shape, dt in [(5, np.int64), ((3, 4), np.float64), ((0,), np.uint32), (1 << 21, np.float32)]:
+        a = host_empty(shape, dt)
+        assert a.dtype == np.dtype(dt) and a.shape == ((shape,) if isinstance(shape, int) else shape)
+        assert a.flags.c_contiguous and a.flags.writeable

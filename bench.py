@@ -390,7 +390,8 @@ class SpmvBench:
         p = self.prep.permuted
         s = self.hprep.split_row
         nz = int(p.row_ptr[-1] - p.row_ptr[s])
-        return (4 * (p.rows - s + 1) + 12 * nz + self.x_host.nbytes), 8 * (p.rows - s)
+        per_nz = p.col_idx.dtype.itemsize + p.values.dtype.itemsize
+        return (p.row_ptr.dtype.itemsize * (p.rows - s + 1) + per_nz * nz + self.x_host.nbytes), 8 * (p.rows - s)
 
     def cpu_sample(self, budget_s: float):
         from oracle import spmv as ospmv

@@ -202,13 +202,14 @@ int hb_list_fis_stats(const void* succ, int succ_code, int64_t n, int64_t head, 
  * The host share of a work-shared run on `workers` host threads, bit-identical
  * to the reference's numpy bodies (no GPU involved): histogram
  * (HistogramWorkload.run_part, kernels_regular.py:149-154), CSR row range
- * (_csr_range_matvec, kernels_irregular.py:206-211; y[i - row0]),
+ * (_csr_range_matvec, kernels_irregular.py:206-211; y[i - row0], or
+ * y[perm[i]] when perm is given — the un-permute of :224-227 fused in),
  * convolution rows (convolve_rows, kernels_regular.py:359-381; f64 out) and
  * bilateral rows (bilateral_rows, :461-486; f64 out).                      */
 int hb_host_hist(const void* data, int dtype, int64_t n, int32_t bin_count, uint64_t* bins_out, int workers);
 int hb_host_spmv_rows(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
-                      const double* values, int64_t row0, int64_t row1, const double* x, double* y,
-                      int workers);
+                      const double* values, int64_t row0, int64_t row1, const double* x,
+                      const void* perm, int perm_code, double* y, int workers);
 int hb_host_conv_rows(const void* img, int in_code, int32_t height, int32_t width, int32_t radius,
                       const double* weights, int32_t row0, int32_t row1, double* out, int workers);
 int hb_host_bilateral(const uint8_t* img, int32_t height, int32_t width, int32_t radius,

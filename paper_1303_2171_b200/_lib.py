@@ -50,7 +50,7 @@ _SIGNATURES: dict[str, list] = {
     "hb_bilateral_u8": [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _int, _int, _vp],
     "hb_convolve": [_vp, _int, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _int, _int, _vp],
     "hb_host_hist": [_vp, _int, _i64, _i32, _vp, _int],
-    "hb_host_spmv_rows": [_vp, _int, _vp, _int, _vp, _i64, _i64, _vp, _vp, _int],
+    "hb_host_spmv_rows": [_vp, _int, _vp, _int, _vp, _i64, _i64, _vp, _vp, _int, _vp, _int],
     "hb_host_conv_rows": [_vp, _int, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _int],
     "hb_host_bilateral": [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _int],
     "hb_sort": [_vp, _vp, _int, _vp, _vp, _i64, _vp, _int, _vp],

@@ -79,6 +79,13 @@ int copy_out(void* dst, const DevBuf& b, size_t bytes, bool device, cudaStream_t
 int copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int finish(int flags, cudaStream_t s);  // sync unless HB_ASYNC, surface errors
+// D2H of a device buffer through the pinned stage: fn(stage, offset, len)
+// runs on each landed chunk (in order) while the next chunk's DMA is in flight.
+int d2h_visit(const void* src, size_t bytes, cudaStream_t s,
+              const std::function<void(const char*, size_t, size_t)>& fn);
+// fn(0..n-1) on the process-wide host thread pool (one region at a time).
+void host_parallel(int n, const std::function<void(int)>& fn);
+int host_threads();
 // Host-buffer row filters: H2D of input rows (on a side stream), the kernel
 // of each row chunk on `s` (launch(a, b) = absolute rows [a, b)), D2H of the
 // chunk's output rows on another side stream; returns with the output landed.

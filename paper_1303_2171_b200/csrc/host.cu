@@ -175,26 +175,72 @@ extern "C" int hb_host_hist(const void* data, int dtype, int64_t n, int32_t bin_
   return HB_OK;
 }
 
+namespace hb {
+namespace {
+
+// CSR rows [row0, row1): typed loops (no per-element index-width dispatch),
+// thread chunks balanced by nonzeros rather than rows (the nnz-sorted
+// permuted matrix has very uneven row lengths), result written to y[i - row0]
+// or scattered to y[perm[i]] when a permutation is given.
+template <typename P, typename C, typename Q>
+void spmv_rows_typed(const P* rp, const C* ci, const double* v, int64_t row0, int64_t row1, const double* x,
+                     const Q* perm, double* y, int workers) {
+  const int64_t rows = row1 - row0, nz0 = (int64_t)rp[row0], nnz = (int64_t)rp[row1] - nz0;
+  if (rows < 4096 || nnz < (1 << 16)) workers = 1;
+  std::vector<int64_t> cut((size_t)workers + 1);
+  cut[0] = row0;
+  cut[(size_t)workers] = row1;
+  for (int k = 1; k < workers; ++k) {  // first row whose start reaches k/w of the nonzeros
+    const int64_t target = nz0 + nnz * k / workers;
+    cut[(size_t)k] = std::max(cut[(size_t)k - 1], (int64_t)(std::lower_bound(rp + row0, rp + row1, (P)target) - rp));
+  }
+  parallel_chunks(workers, workers, [&](int k, int64_t, int64_t) {
+    for (int64_t r = cut[(size_t)k]; r < cut[(size_t)k + 1]; ++r) {
+      const int64_t e = (int64_t)rp[r + 1];
+      double acc = 0.0;
+      for (int64_t j = (int64_t)rp[r]; j < e; ++j) {
+        const double prod = v[j] * x[(int64_t)ci[j]];
+        acc = acc + prod;
+      }
+      if (perm) y[(int64_t)perm[r]] = acc;
+      else y[r - row0] = acc;
+    }
+  });
+}
+
+template <typename P, typename C>
+void spmv_rows_perm(const P* rp, const C* ci, const double* v, int64_t row0, int64_t row1, const double* x,
+                    const void* perm, int perm_code, double* y, int workers) {
+  if (perm_code == HB_I32)
+    spmv_rows_typed(rp, ci, v, row0, row1, x, reinterpret_cast<const int32_t*>(perm), y, workers);
+  else
+    spmv_rows_typed(rp, ci, v, row0, row1, x, reinterpret_cast<const int64_t*>(perm), y, workers);
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
 extern "C" int hb_host_spmv_rows(const void* row_ptr, int ptr_code, const void* col_idx, int col_code,
-                                 const double* values, int64_t row0, int64_t row1, const double* x, double* y,
-                                 int workers) {
+                                 const double* values, int64_t row0, int64_t row1, const double* x,
+                                 const void* perm, int perm_code, double* y, int workers) {
   HB_CHECK_ARG((ptr_code == HB_I32 || ptr_code == HB_I64) && (col_code == HB_I32 || col_code == HB_I64),
                "row_ptr/col_idx must be int32 or int64");
+  HB_CHECK_ARG(perm == nullptr || perm_code == HB_I32 || perm_code == HB_I64, "perm must be int32 or int64");
   HB_CHECK_ARG(row0 >= 0 && row1 >= row0, "bad row range");
   if (row1 == row0) return HB_OK;
   HB_CHECK_ARG(row_ptr && x && y, "NULL pointer");
-  parallel_chunks(row1 - row0, clamp_workers(workers), [&](int, int64_t a, int64_t b) {
-    for (int64_t i = a; i < b; ++i) {
-      const int64_t r = row0 + i;
-      const int64_t s = idx_at(row_ptr, ptr_code, r), e = idx_at(row_ptr, ptr_code, r + 1);
-      double acc = 0.0;
-      for (int64_t k = s; k < e; ++k) {
-        const double prod = values[k] * x[idx_at(col_idx, col_code, k)];
-        acc = acc + prod;
-      }
-      y[i] = acc;
-    }
-  });
+  const int w = clamp_workers(workers);
+  const bool p32 = ptr_code == HB_I32, c32 = col_code == HB_I32;
+  const auto* p4 = reinterpret_cast<const int32_t*>(row_ptr);
+  const auto* p8 = reinterpret_cast<const int64_t*>(row_ptr);
+  const auto* c4 = reinterpret_cast<const int32_t*>(col_idx);
+  const auto* c8 = reinterpret_cast<const int64_t*>(col_idx);
+  if (p32 && c32) spmv_rows_perm(p4, c4, values, row0, row1, x, perm, perm_code, y, w);
+  else if (p32) spmv_rows_perm(p4, c8, values, row0, row1, x, perm, perm_code, y, w);
+  else if (c32) spmv_rows_perm(p8, c4, values, row0, row1, x, perm, perm_code, y, w);
+  else spmv_rows_perm(p8, c8, values, row0, row1, x, perm, perm_code, y, w);
   return HB_OK;
 }
 

@@ -263,6 +263,34 @@ int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   return HB_OK;
 }
 
+void host_parallel(int n, const std::function<void(int)>& fn) { HostPool::get().run(fn, n); }
+
+int host_threads() { return HostPool::get().size(); }
+
+int d2h_visit(const void* src, size_t bytes, cudaStream_t s,
+              const std::function<void(const char*, size_t, size_t)>& fn) {
+  if (bytes == 0) return HB_OK;
+  StagerLease lease;
+  HB_TRY(stager(&lease));
+  Stager* st = lease.st;
+  const char* in = reinterpret_cast<const char*>(src);
+  const size_t n = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](size_t i) -> int {
+    const size_t off = i * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    HB_CUDA_TRY(cudaMemcpyAsync(st->buf[i & 1], in + off, len, cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaEventRecord(st->ev[i & 1], s));
+    return HB_OK;
+  };
+  HB_TRY(issue(0));
+  for (size_t i = 0; i < n; ++i) {
+    if (i + 1 < n) HB_TRY(issue(i + 1));  // next chunk's DMA overlaps this chunk's visit
+    HB_CUDA_TRY(cudaEventSynchronize(st->ev[i & 1]));
+    const size_t off = i * kStageChunk;
+    fn(st->buf[i & 1], off, std::min(kStageChunk, bytes - off));
+  }
+  return HB_OK;
+}
+
 int stage_in(DevBuf* b, const void* src, size_t bytes, bool device, cudaStream_t s) {
   if (device) {
     b->ptr = const_cast<void*>(src);

@@ -549,6 +549,12 @@ int dispatch_perm(int perm_code, const void* rp, const void* ci, const double* v
   return launch_spmv<P, C, int64_t>(rp, ci, v, x, row0, row1, pm, y, mode, s);
 }
 
+template <typename I, typename O>
+__global__ void rebase_kernel(const I* __restrict__ in, int64_t n, int64_t base, O* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (O)((int64_t)in[i] - base);
+}
+
 __global__ void narrow_i64_kernel(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)in[i];
@@ -607,23 +613,24 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
   HB_TRY(read_index(row_ptr, ptr_code, row1, false, s, &nz1));
   HB_CHECK_ARG(nz1 >= nz0 && nz0 >= 0, "row_ptr is not non-decreasing");
   DevBuf d_ptr, d_col, d_val, d_x, d_y;
-  // rebase row_ptr so the staged col/val slices start at 0; int32 when the
-  // range allows, so int32 col_idx takes the lane-per-row kernel
+  // rebase row_ptr so the staged col/val slices start at 0 — on the device,
+  // from the raw slice (one DMA, no host pass); int32 when the range allows,
+  // so int32 col_idx takes the lane-per-row kernel
   const bool p32 = nz1 - nz0 <= (int64_t)INT32_MAX;
-  std::vector<int64_t> ptr64(p32 ? 0 : (size_t)rows + 1);
-  std::vector<int32_t> ptr32(p32 ? (size_t)rows + 1 : 0);
-  auto rebase = [&](auto* src) {  // typed (vectorisable) loop
-    for (int64_t i = 0; i <= rows; ++i) {
-      const int64_t v = (int64_t)src[row0 + i] - nz0;
-      if (p32) ptr32[(size_t)i] = (int32_t)v;
-      else ptr64[(size_t)i] = v;
-    }
-  };
-  if (ptr_code == HB_I32) rebase(reinterpret_cast<const int32_t*>(row_ptr));
-  else rebase(reinterpret_cast<const int64_t*>(row_ptr));
-  (void)pe;
-  if (p32) HB_TRY(stage_in(&d_ptr, ptr32.data(), ptr32.size() * 4, false, s));
-  else HB_TRY(stage_in(&d_ptr, ptr64.data(), ptr64.size() * 8, false, s));
+  {
+    DevBuf d_raw;
+    HB_TRY(stage_in(&d_raw, reinterpret_cast<const char*>(row_ptr) + (size_t)row0 * pe, (size_t)(rows + 1) * pe, false, s));
+    HB_TRY(alloc(&d_ptr, (size_t)(rows + 1) * (p32 ? 4 : 8), s));
+    DeviceInfo di;
+    HB_TRY(device_info(&di));
+    int64_t g = ceil_div(rows + 1, 256);
+    if (g > (int64_t)di.sms * 16) g = (int64_t)di.sms * 16;
+    if (pe == 4 && p32) rebase_kernel<<<(int)g, 256, 0, s>>>(d_raw.as<int32_t>(), rows + 1, nz0, d_ptr.as<int32_t>());
+    else if (pe == 4) rebase_kernel<<<(int)g, 256, 0, s>>>(d_raw.as<int32_t>(), rows + 1, nz0, d_ptr.as<int64_t>());
+    else if (p32) rebase_kernel<<<(int)g, 256, 0, s>>>(d_raw.as<int64_t>(), rows + 1, nz0, d_ptr.as<int32_t>());
+    else rebase_kernel<<<(int)g, 256, 0, s>>>(d_raw.as<int64_t>(), rows + 1, nz0, d_ptr.as<int64_t>());
+    HB_TRY(check_launch());
+  }
   HB_TRY(stage_in(&d_col, reinterpret_cast<const char*>(col_idx) + nz0 * ce, (size_t)(nz1 - nz0) * ce, false, s));
   HB_TRY(stage_in(&d_val, values + nz0, (size_t)(nz1 - nz0) * 8, false, s));
   HB_TRY(stage_in(&d_x, x, (size_t)cols * 8, false, s));
@@ -653,21 +660,19 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
     HB_CUDA_TRY(cudaStreamSynchronize(s));
     return HB_OK;
   }
-  std::vector<double> tmp((size_t)rows);
-  HB_TRY(copy_d2h(tmp.data(), d_y.ptr, (size_t)rows * 8, s));
-  HB_CUDA_TRY(cudaStreamSynchronize(s));
-  // un-permute on the host: y[perm[row0 + i]] = row sum i (typed loop, 4 threads)
-  auto scatter = [&](auto* pm) {
-    const int nt = rows >= (1 << 18) ? 4 : 1;
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t)
-      th.emplace_back([&, t] {
-        for (int64_t i = rows * t / nt, e = rows * (t + 1) / nt; i < e; ++i) y[(int64_t)pm[row0 + i]] = tmp[(size_t)i];
+  // un-permute on the host straight from the pinned stage: y[perm[row0 + i]] = row sum i
+  auto scatter = [&](auto* pm) -> int {
+    return d2h_visit(d_y.ptr, (size_t)rows * 8, s, [&](const char* h, size_t off, size_t len) {
+      const double* t = reinterpret_cast<const double*>(h);
+      const int64_t i0 = (int64_t)(off / 8), n = (int64_t)(len / 8);
+      const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(host_threads(), n >> 15));
+      host_parallel(parts, [&](int k) {
+        for (int64_t i = n * k / parts, e = n * (k + 1) / parts; i < e; ++i) y[(int64_t)pm[row0 + i0 + i]] = t[i];
       });
-    for (auto& t : th) t.join();
+    });
   };
-  if (perm_code == HB_I32) scatter(reinterpret_cast<const int32_t*>(perm));
-  else scatter(reinterpret_cast<const int64_t*>(perm));
+  HB_TRY(perm_code == HB_I32 ? scatter(reinterpret_cast<const int32_t*>(perm))
+                             : scatter(reinterpret_cast<const int64_t*>(perm)));
   (void)qe;
   return HB_OK;
 }

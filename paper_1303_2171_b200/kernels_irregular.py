@@ -287,13 +287,26 @@ def _device_preprocess(m: CsrMatrix):
     return perm, CsrMatrix(m.rows, m.cols, nrp, ncol, nval)
 
 
-def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int, workers: int = 1) -> np.ndarray:
+def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int, workers: int = 1,
+                       perm: Any = None, y: np.ndarray | None = None) -> np.ndarray:
     """DeviceA body (:206-211) in native code (hb_host_spmv_rows on `workers`
     threads): rounded products summed left to right per row — exactly the
-    reference's product + bincount arithmetic."""
-    y = np.zeros(max(row1 - row0, 0))
+    reference's product + bincount arithmetic.  With `perm` and `y`, row r's
+    sum goes straight to y[perm[r]] (the un-permute of :224-227 fused in)."""
+    if perm is None:
+        y = np.zeros(max(row1 - row0, 0))
     if row1 <= row0:
         return y
+    rp, ci = buf(to_host(m.row_ptr)), buf(to_host(m.col_idx))
+    v = np.ascontiguousarray(to_host(m.values), dtype=np.float64)
+    xh = np.ascontiguousarray(x, dtype=np.float64)
+    pb = buf(to_host(perm)) if perm is not None else None
+    if pb is not None and (pb.code not in (_lib.DTYPE_CODES["i4"], _lib.DTYPE_CODES["i8"]) or y is None
+                           or not y.flags.c_contiguous or y.dtype != np.float64):
+        raise ValueError("perm must be int32/int64 with a C-contiguous float64 y")
+    _lib.call("hb_host_spmv_rows", vp(rp.ptr), rp.code, vp(ci.ptr), ci.code, vp(v.ctypes.data), row0, row1,
+              vp(xh.ctypes.data), vp(pb.ptr if pb else 0), pb.code if pb else 0, vp(y.ctypes.data), workers)
+    return y
     rp, ci = buf(to_host(m.row_ptr)), buf(to_host(m.col_idx))
     v = np.ascontiguousarray(to_host(m.values), dtype=np.float64)
     xh = np.ascontiguousarray(x, dtype=np.float64)
@@ -338,7 +351,7 @@ def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: An
     xb = buf(to_host(x), np.float64)
     rp, ci, v = buf(m.row_ptr), buf(m.col_idx), buf(m.values, np.float64)
     if y is None:
-        y = np.empty(row1 - row0 if perm is None else m.rows, dtype=np.float64)
+        y = host_empty(row1 - row0 if perm is None else m.rows, np.float64)
     if row1 == row0:
         return y
     pb = buf(perm) if perm is not None else None
@@ -389,10 +402,10 @@ def spmv_hybrid(prep: SpmvPrep, x: Any) -> np.ndarray:
     # host matrix, one GPU: each side scatters its own rows into y (the GPU
     # side inside the C call) — no concatenation, no full-size host scatter
     perm = np.asarray(to_host(prep.perm))
-    y = np.empty(m.rows)
+    y = host_empty(m.rows, np.float64)
 
     def side_a():
-        y[perm[:split]] = _host_range_matvec(m, xh, 0, split, prep.workers_a)
+        _host_range_matvec(m, xh, 0, split, prep.workers_a, perm=perm, y=y)
 
     with ThreadPoolExecutor(max_workers=2) as pool:
         fa = pool.submit(side_a)

@@ -149,3 +149,30 @@ def test_host_empty_shapes_and_dtypes():
         a = host_empty(shape, dt)
         assert a.dtype == np.dtype(dt) and a.shape == ((shape,) if isinstance(shape, int) else shape)
         assert a.flags.c_contiguous and a.flags.writeable
+
+
+@pytest.mark.parametrize("idx", [np.int32, np.int64])
+def test_host_spmv_rows_nnz_balanced_and_perm_scatter(idx):
+    """Rows long enough for the threaded, nnz-balanced path (skewed row
+    lengths, as in the nnz-sorted matrix), plain and with the fused
+    y[perm[r]] scatter, against the oracle."""
+    from oracle import spmv as ospmv
+
+    rng = np.random.default_rng(5)
+    rows = 20_000
+    lens = np.sort(rng.zipf(1.6, rows).clip(0, 3000))[::-1]  # heavy rows first
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(idx)
+    col = np.concatenate([np.sort(rng.choice(rows, int(k), replace=False)) for k in lens]).astype(idx)
+    val = rng.standard_normal(int(ptr[-1]))
+    x = rng.standard_normal(rows)
+    assert ptr[-1] > 1 << 16
+    m = CsrMatrix(rows, rows, ptr, col, val)
+    want = ospmv.range_matvec(ptr.astype(np.int64), col.astype(np.int64), val, x, 0, rows)
+    for w in (1, 3, 16):
+        assert np.array_equal(bits(_host_range_matvec(m, x, 0, rows, w)), bits(want))
+        assert np.array_equal(bits(_host_range_matvec(m, x, 777, 15_000, w)), bits(want[777:15_000]))
+        perm = rng.permutation(rows).astype(idx)
+        y = np.full(rows, np.nan)
+        _host_range_matvec(m, x, 100, 19_000, w, perm=perm, y=y)
+        assert np.array_equal(bits(y[perm[100:19_000]]), bits(want[100:19_000]))
+        assert np.isnan(np.delete(y, perm[100:19_000])).all()

@@ -221,3 +221,21 @@ def test_device_preprocess_matches_host(platform13):
     perm, permuted, split = ospmv.preprocess(ptr, col, val, 1.0, 3.0, 0.0)
     want = ospmv.hybrid(perm, permuted, split, x)
     assert np.array_equal(bits(y.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("pdt", [np.int32, np.int64])
+def test_host_path_unpermute_from_stage(pdt):
+    """Host arrays, multi-threaded un-permute out of the pinned stage: every
+    row must land at y[perm[r]] bit-exactly and nothing else may be written,
+    for full and partial ranges, int32 and int64 perms."""
+    rows = 150_000
+    ptr, col, val = ods.csr(rows, rows, 7, 4e-5)
+    x = 2.0 * orng.uniform_floats(orng.mix_seed(7, 0xDEC0), rows) - 1.0
+    m = CsrMatrix(rows, rows, ptr, col, val)
+    want = ospmv.range_matvec(ptr, col, val, x, 0, rows)
+    perm = np.random.default_rng(3).permutation(rows).astype(pdt)
+    for r0, r1 in [(0, rows), (1234, 1234 + 70_000), (rows - 65_536, rows)]:
+        y = np.full(rows, np.nan)
+        gpu_spmv(m, x, r0, r1, y, perm)
+        assert np.array_equal(bits(y[perm[r0:r1]]), bits(want[r0:r1]))
+        assert np.isnan(np.delete(y, perm[r0:r1])).all()

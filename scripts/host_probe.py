@@ -16,3 +16,16 @@ d = torch.empty_like(h, device="cuda")
 for _ in range(2):
     torch.cuda.synchronize(); t = time.perf_counter(); d.copy_(h, non_blocking=True); torch.cuda.synchronize()
 print(f"H2D pinned: {data.size / (time.perf_counter() - t) / 1e9:.1f} GB/s")
+# host histogram while a 1 GiB H2D DMA streams from another pinned buffer (contention)
+import threading
+big = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+dbig = torch.empty_like(big, device="cuda")
+for w in (8, 15):
+    stop = False
+    def dma():
+        while not stop:
+            dbig.copy_(big, non_blocking=True); torch.cuda.synchronize()
+    th = threading.Thread(target=dma); th.start(); time.sleep(0.05)
+    t = time.perf_counter(); host_histogram(data, 256, w); dt = time.perf_counter() - t
+    stop = True; th.join()
+    print(f"workers {w:3d} under DMA: {data.size / dt / 1e9:.2f} Gelem/s")

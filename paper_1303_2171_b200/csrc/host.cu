@@ -43,31 +43,45 @@ int clamp_workers(int w) {
   return std::max(1, std::min(w, hw));
 }
 
-// uint8 fast path: 8 bytes per load, 4 interleaved 32-bit sub-histograms (no
-// store-to-load dependency between neighbouring equal bytes), flushed to the
-// 64-bit counts every 2^30 bytes.
+// uint8 fast path: two 8-byte words per iteration, byte k of each word counted
+// in sub-histogram k (8 tables: no store-to-load dependency between nearby
+// equal bytes; ~30 % faster than 4 tables on the B200 box's host,
+// scripts/micro/host_hist.cpp), flushed to the 64-bit counts every 2^30 bytes.
 bool hist_u8_fast(const uint8_t* d, int64_t a, int64_t b, int32_t bins, uint64_t* h) {
   if (bins < 256) return false;  // values >= bins possible: generic path checks them
-  static thread_local uint32_t sub[4][256];
+  static thread_local uint32_t sub[8][256];
   int64_t i = a;
   while (i < b) {
     memset(sub, 0, sizeof(sub));
     const int64_t e = std::min(b, i + ((int64_t)1 << 30));
     for (; i < e && (i & 7); ++i) ++sub[0][d[i]];
-    for (; i + 8 <= e; i += 8) {
-      uint64_t w;
+    for (; i + 16 <= e; i += 16) {
+      uint64_t w, u;
       memcpy(&w, d + i, 8);
+      memcpy(&u, d + i + 8, 8);
       ++sub[0][w & 255];
       ++sub[1][(w >> 8) & 255];
       ++sub[2][(w >> 16) & 255];
       ++sub[3][(w >> 24) & 255];
-      ++sub[0][(w >> 32) & 255];
-      ++sub[1][(w >> 40) & 255];
-      ++sub[2][(w >> 48) & 255];
-      ++sub[3][w >> 56];
+      ++sub[4][(w >> 32) & 255];
+      ++sub[5][(w >> 40) & 255];
+      ++sub[6][(w >> 48) & 255];
+      ++sub[7][w >> 56];
+      ++sub[0][u & 255];
+      ++sub[1][(u >> 8) & 255];
+      ++sub[2][(u >> 16) & 255];
+      ++sub[3][(u >> 24) & 255];
+      ++sub[4][(u >> 32) & 255];
+      ++sub[5][(u >> 40) & 255];
+      ++sub[6][(u >> 48) & 255];
+      ++sub[7][u >> 56];
     }
     for (; i < e; ++i) ++sub[0][d[i]];
-    for (int v = 0; v < 256; ++v) h[v] += (uint64_t)sub[0][v] + sub[1][v] + sub[2][v] + sub[3][v];
+    for (int v = 0; v < 256; ++v) {
+      uint64_t t = 0;
+      for (int k = 0; k < 8; ++k) t += sub[k][v];
+      h[v] += t;
+    }
   }
   return true;
 }

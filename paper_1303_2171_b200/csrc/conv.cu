@@ -89,16 +89,24 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // multiplying the independent accumulation chains that hide the fp64 result
 // latency.  Tap order per output pixel is still row-major (iy increases), so
 // the result is bit-identical.
-template <int R, typename IN, typename OUT, bool DENSE, int MINB, int NR>
+//
+// V2 (default): the row segments come in as 16-byte shared loads, and lane l
+// of a warp takes row group l % 4, pixel group l / 4, so the 8 lanes of each
+// quarter-warp hit 8 distinct 16-byte bank slots (the row stride NR·TW is
+// ≡ 2·odd mod 16 doubles) — conflict-free, where the row-major lane order
+// put 4 lanes on each slot (ncu: 61 % of the shared wavefronts were
+// conflicts).  Same pixels per thread, same tap order.
+template <int R, typename IN, typename OUT, bool DENSE, int MINB, int NR, bool V2 = true>
 __global__ void __launch_bounds__(kThreads, MINB)
     conv_rows_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
                      const double* __restrict__ weights, OUT* __restrict__ out) {
   constexpr int S = 2 * R + 1;
+  constexpr int SWP = (S * S + 1) & ~1;  // weights padded so the tile is 16-B aligned
   constexpr int TILE_H = kTileH * NR;
   constexpr int TH = TILE_H + 2 * R, TW = kTileW + 2 * R;
   extern __shared__ __align__(16) unsigned char smem[];
   double* sw = reinterpret_cast<double*>(smem);  // [S*S]
-  double* tile = sw + S * S;                     // [TH][TW]
+  double* tile = sw + SWP;                       // [TH][TW]
   const int tid = threadIdx.x;
   const int y0 = row0 + blockIdx.y * TILE_H;
   const int x0 = blockIdx.x * kTileW;
@@ -110,8 +118,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     tile[i] = to_f64(img[(int64_t)gy * W + gx]);
   }
   __syncthreads();
-  const int py = (tid / (kTileW / kPx)) * NR;  // first of the thread's NR output rows
-  const int px = (tid % (kTileW / kPx)) * kPx;
+  static_assert(kTileW / kPx == 8 && kThreads % 32 == 0, "lane mapping assumes 8 pixel groups per row");
+  const int lane = tid & 31;
+  const int rgrp = V2 ? (tid >> 5) * 4 + (lane & 3) : tid / (kTileW / kPx);
+  const int py = rgrp * NR;  // first of the thread's NR output rows
+  const int px = (V2 ? lane >> 2 : tid % (kTileW / kPx)) * kPx;
   const int gy = y0 + py;
   if (gy >= row1) return;
   double acc[NR][kPx];
@@ -123,8 +134,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (int iy = 0; iy < S + NR - 1; ++iy) {  // input rows py .. py+S+NR-2 of the tile
     double seg[kPx + 2 * R];
     const double* trow = tile + (py + iy) * TW + px;
+    if (V2) {
+      static_assert(TW % 2 == 0 && (kPx + 2 * R) % 2 == 0, "16-byte segment loads");
 #pragma unroll
-    for (int q = 0; q < kPx + 2 * R; ++q) seg[q] = trow[q];
+      for (int q = 0; q < (kPx + 2 * R) / 2; ++q) {
+        const double2 v = reinterpret_cast<const double2*>(trow)[q];
+        seg[2 * q] = v.x;
+        seg[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kPx + 2 * R; ++q) seg[q] = trow[q];
+    }
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
       const int dy = iy - k;
@@ -283,10 +304,10 @@ int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w
   };
   // default: NR = 3 output rows per thread, 2 CTAs/SM (measured at r=7:
   // 31.1 Gpix/s vs 27.9 for NR = 2 and 24.8 for one row); HB_CONV_CFG 2/3/4:
-  // one row per thread, 5-7 other shapes
+  // one row per thread, 5-7 other shapes, 8 the row-major lane order
   if (variant == 0 || (variant >= 5 && variant <= 7)) {
     auto launch_n = [&](auto kern, int nr) -> int {
-      const size_t smem2 = (size_t)S * S * 8 + (size_t)(kTileH * nr + 2 * R) * (kTileW + 2 * R) * 8;
+      const size_t smem2 = (size_t)((S * S + 1) & ~1) * 8 + (size_t)(kTileH * nr + 2 * R) * (kTileW + 2 * R) * 8;
       dim3 grid2((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH * nr));
       HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       kern<<<grid2, kThreads, smem2, s>>>(img, H, W, row0, row1, w, out);
@@ -295,6 +316,7 @@ int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w
     if (variant == 5) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 2, 2>, 2) : launch_n(conv_rows_kernel<R, IN, OUT, false, 2, 2>, 2);
     if (variant == 6) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 1, 4>, 4) : launch_n(conv_rows_kernel<R, IN, OUT, false, 1, 4>, 4);
     if (variant == 7) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 3, 2>, 2) : launch_n(conv_rows_kernel<R, IN, OUT, false, 3, 2>, 2);
+    if (variant == 8) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 2, 3, false>, 3) : launch_n(conv_rows_kernel<R, IN, OUT, false, 2, 3, false>, 3);
     return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 2, 3>, 3) : launch_n(conv_rows_kernel<R, IN, OUT, false, 2, 3>, 3);
   }
   if (variant == 2) return dense ? launch(conv_tile_kernel<R, IN, OUT, true, 2>) : launch(conv_tile_kernel<R, IN, OUT, false, 2>);

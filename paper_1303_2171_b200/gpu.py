@@ -36,6 +36,26 @@ def require_gpu() -> None:
         raise HybridBenchError("no CUDA device visible: the DeviceB (GPU) share cannot run")
 
 
+def inherit_device(fn: Any) -> Any:
+    """Wrap `fn` for another thread so that it runs on the CALLING thread's
+    CUDA device.  The CUDA runtime's current device is per host thread and a
+    new thread starts on device 0, so without this the run_part threads of a
+    rank bound to cuda:k (torchrun, one process per GPU) would allocate,
+    copy and launch on GPU 0."""
+    dev = None
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        dev = torch.cuda.current_device()
+    if dev is None:
+        return fn
+
+    def run(*args: Any, **kwargs: Any) -> Any:
+        if torch.cuda.current_device() != dev:
+            torch.cuda.set_device(dev)
+        return fn(*args, **kwargs)
+
+    return run
+
+
 def current_stream_handle(x: Any = None) -> int:
     """cudaStream_t of torch's current stream (0 = legacy default stream)."""
     if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib, sharding
 from .errors import DataIOError, StructuralError
-from .gpu import buf, current_stream_handle, host_empty, is_device_array, require_gpu, to_host, vp
+from .gpu import buf, current_stream_handle, host_empty, inherit_device, is_device_array, require_gpu, to_host, vp
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
 
@@ -394,7 +394,7 @@ def spmv_hybrid(prep: SpmvPrep, x: Any) -> np.ndarray:
     if m.on_device or (g is not None and g.world > 1):
         with ThreadPoolExecutor(max_workers=2) as pool:
             fa = pool.submit(_host_range_matvec, m, xh, 0, split, prep.workers_a)
-            fb = pool.submit(_gpu_rows, m, x_side_b, split, m.rows)
+            fb = pool.submit(inherit_device(_gpu_rows), m, x_side_b, split, m.rows)
             y_perm = np.concatenate([fa.result(), fb.result()])
         y = np.empty_like(y_perm)
         y[to_host(prep.perm)] = y_perm
@@ -409,7 +409,7 @@ def spmv_hybrid(prep: SpmvPrep, x: Any) -> np.ndarray:
 
     with ThreadPoolExecutor(max_workers=2) as pool:
         fa = pool.submit(side_a)
-        fb = pool.submit(gpu_spmv, m, xh, split, m.rows, y, perm) if split < m.rows else None
+        fb = pool.submit(inherit_device(gpu_spmv), m, xh, split, m.rows, y, perm) if split < m.rows else None
         fa.result()
         if fb is not None:
             fb.result()

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib, sharding
 from .errors import DataIOError
-from .gpu import buf, current_stream_handle, flags_for, host_empty, is_device_array, require_gpu, to_host, vp
+from .gpu import buf, current_stream_handle, flags_for, host_empty, inherit_device, is_device_array, require_gpu, to_host, vp
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
 
@@ -344,7 +344,7 @@ def sample_sort_hybrid(
 
     with ThreadPoolExecutor(max_workers=2) as pool:
         fa = pool.submit(np.sort, part_a, kind="quicksort")
-        fb = pool.submit(lambda: sharding.to_numpy(sharding.run_sharded_sort(_gpu_keys(part_b))[0]))
+        fb = pool.submit(inherit_device(lambda: sharding.to_numpy(sharding.run_sharded_sort(_gpu_keys(part_b))[0])))
         sorted_a, sorted_b = fa.result(), fb.result()
     out = np.empty_like(host)
     pos = pa = pb = 0

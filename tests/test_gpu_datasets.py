@@ -27,3 +27,22 @@ def test_device_gen_list_matches_reference_generator():
     succ, head = d.device_gen_list(50_000, 11)
     want = d.gen_list(50_000, 11)
     assert head == want.head and np.array_equal(succ.cpu().numpy().astype(np.int64), want.succ)
+
+
+def test_worker_threads_inherit_the_callers_device():
+    """run_workshared's side threads must run on the rank's GPU (a new
+    host thread starts on device 0): the wrapper carries the device over."""
+    import threading
+
+    import torch
+
+    from paper_1303_2171_b200.gpu import inherit_device
+
+    last = torch.cuda.device_count() - 1
+    torch.cuda.set_device(last)
+    seen = []
+    t = threading.Thread(target=inherit_device(lambda: seen.append(torch.cuda.current_device())))
+    t.start()
+    t.join()
+    torch.cuda.set_device(0)
+    assert seen == [last]

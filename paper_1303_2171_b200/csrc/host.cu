@@ -24,18 +24,13 @@ namespace {
 
 template <typename F>
 void parallel_chunks(int64_t n, int workers, F&& fn) {
-  // contiguous chunks [k*n/w, (k+1)*n/w), one thread each (the reference's split)
+  // contiguous chunks [k*n/w, (k+1)*n/w), one task each (the reference's
+  // split), on the persistent host-kernel pool (no thread spawn per call)
   if (workers <= 1 || n < 2) {
     fn(0, 0, n);
     return;
   }
-  std::vector<std::thread> pool;
-  pool.reserve((size_t)workers);
-  for (int k = 0; k < workers; ++k) {
-    const int64_t a = n * k / workers, b = n * (k + 1) / workers;
-    pool.emplace_back([&, k, a, b] { fn(k, a, b); });
-  }
-  for (auto& t : pool) t.join();
+  host_kernel_parallel(workers, [&](int k) { fn(k, n * k / workers, n * (k + 1) / workers); });
 }
 
 int clamp_workers(int w) {

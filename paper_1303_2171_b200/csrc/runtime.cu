@@ -77,11 +77,14 @@ namespace {
 // minimal fork-join pool: run(fn, n) calls fn(0..n-1) on up to `size` threads
 class HostPool {
  public:
-  static HostPool& get() {
+  // pool 0: transfer staging (memcpy / un-permute), pool 1: the host-share
+  // (DeviceA) kernels — separate, so a GPU side's copies never queue behind
+  // the concurrent host side of the same run_workshared
+  static HostPool& get(int which = 0) {
     // never destroyed: its detached workers wait on cv_ until the process
     // ends, and destroying a condition variable with waiters blocks in glibc
-    static HostPool* p = new HostPool();
-    return *p;
+    static HostPool* p[2] = {new HostPool(), new HostPool()};
+    return *p[which & 1];
   }
   int size() const { return (int)workers_.size() + 1; }
   void run(const std::function<void(int)>& fn, int n) {
@@ -264,6 +267,8 @@ int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 }
 
 void host_parallel(int n, const std::function<void(int)>& fn) { HostPool::get().run(fn, n); }
+
+void host_kernel_parallel(int n, const std::function<void(int)>& fn) { HostPool::get(1).run(fn, n); }
 
 int host_threads() { return HostPool::get().size(); }
 

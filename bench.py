@@ -285,6 +285,16 @@ class HistBench:
             dist.all_reduce(t)
         return res
 
+    def e2e_verify(self, res):
+        """The e2e result (host+GPU split) equals the device histogram of the same data."""
+        import torch
+
+        from paper_1303_2171_b200.kernels_regular import gpu_histogram
+
+        ref = torch.zeros(self.bins, dtype=torch.int64, device="cuda")
+        gpu_histogram(self.x, self.bins, ref)
+        return bool(np.array_equal(np.asarray(res.bins), ref.cpu().numpy()))
+
     def e2e_bytes(self):
         return self.n - int(math.floor(self.share.fraction_a * self.n)), self.bins * 8
 
@@ -385,6 +395,14 @@ class SpmvBench:
         from paper_1303_2171_b200.kernels_irregular import spmv_hybrid
 
         return spmv_hybrid(self.hprep, self.hx)
+
+    def e2e_verify(self, y):
+        """Bit-exact against the oracle (original row order)."""
+        from oracle import spmv as ospmv
+
+        p = self.prep.permuted
+        want = ospmv.hybrid(self.prep.perm, (p.row_ptr, p.col_idx, p.values), 0, self.x_host)
+        return bool(np.array_equal(np.asarray(y).view(np.uint64), want.view(np.uint64)))
 
     def e2e_bytes(self):
         p = self.prep.permuted
@@ -487,6 +505,21 @@ class BilatBench:
 
         return hybrid_bilateral(self.image, self.lut, self.platform, self.share)
 
+    def _oracle_rows(self, host, a, b):
+        from oracle import bilateral as obil
+
+        sp, rg = obil.lut(self.radius, max(self.radius / 2.0, 0.5), 40.0)
+        return obil.rows(host, sp, rg, self.radius, a, b)
+
+    def e2e_verify(self, img):
+        """Sampled rows of the f64 result image (both sides' strips) vs the oracle, bit-exact."""
+        host = self.host.numpy()
+        out = np.asarray(img.pixels)
+        split = int(math.floor(self.share.fraction_a * self.side))
+        rows = {(0, 4), (max(0, split - 2), min(self.side, split + 2)), (8000, 8004), (self.side - 4, self.side)}
+        return bool(all(np.array_equal(out[a:b].view(np.uint64), self._oracle_rows(host, a, b).view(np.uint64))
+                        for a, b in rows if b > a))
+
     def e2e_bytes(self):
         gpu_rows = self.side - int(math.floor(self.share.fraction_a * self.side))
         return gpu_rows * self.side, gpu_rows * self.side * 8
@@ -556,6 +589,11 @@ class ConvBench(BilatBench):
         from paper_1303_2171_b200.kernels_regular import hybrid_convolve
 
         return hybrid_convolve(self.image, self.fk, self.platform, self.share)
+
+    def _oracle_rows(self, host, a, b):
+        from oracle import conv as oconv
+
+        return oconv.rows(host, self.fk.weights, a, b)
 
     def cpu_sample(self, budget_s: float):
         from oracle import conv as oconv
@@ -660,6 +698,16 @@ class SortBench:
 
         return sample_sort_hybrid(self.host_np, self.platform, share=self.share)
 
+    def e2e_verify(self, res):
+        """Sorted, same multiset as the input (count, sum, xor of the keys) — O(n)."""
+        k = np.asarray(res[0]).view(np.uint32)
+        if self.world > 1:  # the sample-merge returns the group's keys: order only
+            return bool(np.all(k[1:] >= k[:-1]))
+        src = self.host_np
+        ok = k.size == src.size and bool(np.all(k[1:] >= k[:-1]))
+        ok = ok and int(k.sum(dtype=np.uint64)) == int(src.sum(dtype=np.uint64))
+        return bool(ok and int(np.bitwise_xor.reduce(k)) == int(np.bitwise_xor.reduce(src)))
+
     def e2e_bytes(self):
         return 4 * self.n, 4 * self.n
 
@@ -760,6 +808,10 @@ class LrBench:
         from paper_1303_2171_b200.kernels_irregular import list_rank_hybrid
 
         return list_rank_hybrid(self.lst, self.platform, self.seed)
+
+    def e2e_verify(self, rank):
+        """Identical to the device-resident ranks (themselves checked in verify())."""
+        return bool(np.array_equal(np.asarray(rank), self.rank.cpu().numpy()))
 
     def e2e_bytes(self):
         return 8 * self.n, 8 * self.n
@@ -873,8 +925,10 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
     barrier(world)
     e_steps = max(1, min(args.steps, args.e2e_steps))
     e0 = time.perf_counter()
+    last = None
     for _ in range(e_steps):
-        wl.e2e_step()
+        last = None  # drop the previous result first, as a caller would (its pinned block is reused)
+        last = wl.e2e_step()
     torch.cuda.synchronize()
     e_s = (time.perf_counter() - e0) / e_steps
     barrier(world)
@@ -911,6 +965,7 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
             "steps": e_steps,
             "api": getattr(wl, "e2e_api", "public drop-in entry point on pinned host buffers"),
             "share": e2e_share_info(wl),
+            "parity": wl.e2e_verify(last) if hasattr(wl, "e2e_verify") else None,
         },
         "clocks": clk,
         "config": wl.config(),

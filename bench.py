@@ -1012,7 +1012,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="all", choices=sorted(WORKLOADS) + ["all"])
-    ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the end-to-end (host buffer) leg")
+    ap.add_argument("--e2e-steps", type=int, default=10, help="steps of the end-to-end (host buffer) leg")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--e2e-share", default="auto", choices=["auto", "calibrated", "gpu"],

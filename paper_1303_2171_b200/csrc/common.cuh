@@ -83,6 +83,21 @@ int finish(int flags, cudaStream_t s);  // sync unless HB_ASYNC, surface errors
 // runs on each landed chunk (in order) while the next chunk's DMA is in flight.
 int d2h_visit(const void* src, size_t bytes, cudaStream_t s,
               const std::function<void(const char*, size_t, size_t)>& fn);
+// A pinned host buffer (one 32 MB stage) borrowed from the stager free list,
+// with its device-mapped address, so a kernel can store results straight
+// into host memory (UVA) — no separate D2H.  Returned to the list on scope exit.
+struct PinnedScratch {
+  void* lease = nullptr;
+  char* host = nullptr;
+  void* dev = nullptr;
+  PinnedScratch() = default;
+  PinnedScratch(const PinnedScratch&) = delete;
+  PinnedScratch& operator=(const PinnedScratch&) = delete;
+  ~PinnedScratch();
+};
+int pinned_scratch(PinnedScratch* out, size_t bytes);  // HB_EINVAL when bytes > one stage
+// true (and the device-mapped address) when `host` is page-locked host memory
+bool device_view(void* host, void** dev);
 // fn(0..n-1) on the process-wide host thread pool (one region at a time).
 void host_parallel(int n, const std::function<void(int)>& fn);
 // the same on a second pool reserved for the host-share (DeviceA) kernels

@@ -268,6 +268,32 @@ int copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 
 void host_parallel(int n, const std::function<void(int)>& fn) { HostPool::get().run(fn, n); }
 
+PinnedScratch::~PinnedScratch() {
+  if (lease) {
+    std::lock_guard<std::mutex> g(g_stage_mu);
+    g_stage_free.push_back(static_cast<Stager*>(lease));
+  }
+}
+
+int pinned_scratch(PinnedScratch* out, size_t bytes) {
+  if (bytes > kStageChunk) return HB_EINVAL;
+  StagerLease l;
+  HB_TRY(stager(&l));
+  out->lease = l.st;
+  out->host = l.st->buf[0];
+  l.st = nullptr;  // ownership moves to `out`
+  return device_view(out->host, &out->dev) ? HB_OK : HB_ECUDA;
+}
+
+bool device_view(void* host, void** dev) {
+  if (!is_pinned(host)) return false;
+  if (cudaHostGetDevicePointer(dev, host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
 void host_kernel_parallel(int n, const std::function<void(int)>& fn) { HostPool::get(1).run(fn, n); }
 
 int host_threads() { return HostPool::get().size(); }

@@ -634,10 +634,23 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
   HB_TRY(stage_in(&d_col, reinterpret_cast<const char*>(col_idx) + nz0 * ce, (size_t)(nz1 - nz0) * ce, false, s));
   HB_TRY(stage_in(&d_val, values + nz0, (size_t)(nz1 - nz0) * 8, false, s));
   HB_TRY(stage_in(&d_x, x, (size_t)cols * 8, false, s));
-  HB_TRY(alloc(&d_y, (size_t)rows * 8, s));
+  // result rows go straight into page-locked host memory when there is some
+  // (the caller's pinned y, or a pinned stage for the un-permute): the
+  // kernel's coalesced y stores cross PCIe while it runs, which avoids a
+  // separate D2H — whose first pass over freshly written device memory
+  // measured ~1 ms for 8 MB here instead of 0.15 ms
+  PinnedScratch scratch;
+  void* ydev = nullptr;
+  bool direct = false;
+  if (perm == nullptr) direct = device_view(y, &ydev);
+  else if ((size_t)rows * 8 <= ((size_t)32 << 20) && pinned_scratch(&scratch, (size_t)rows * 8) == HB_OK) {
+    ydev = scratch.dev;
+    direct = true;
+  }
+  if (!direct) HB_TRY(alloc(&d_y, (size_t)rows * 8, s));
   const double* dv = d_val.as<double>();
   const double* dx = d_x.as<double>();
-  double* dy = d_y.as<double>();
+  double* dy = direct ? reinterpret_cast<double*>(ydev) : d_y.as<double>();
   int rc;
   DevBuf d_col32;
   if (p32 && col_code == HB_I64 && cols <= (int64_t)INT32_MAX && nz1 > nz0) {
@@ -656,8 +669,21 @@ extern "C" int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_id
                                : launch_spmv<int64_t, int64_t, int64_t>(d_ptr.ptr, d_col.ptr, dv, dx, 0, rows, nullptr, dy, mode, s);
   if (rc != HB_OK) return rc;
   if (perm == nullptr) {
-    HB_TRY(copy_d2h(y, d_y.ptr, (size_t)rows * 8, s));
+    if (!direct) HB_TRY(copy_d2h(y, d_y.ptr, (size_t)rows * 8, s));
     HB_CUDA_TRY(cudaStreamSynchronize(s));
+    return HB_OK;
+  }
+  if (direct) {  // un-permute from the pinned rows the kernel wrote
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    const double* t = reinterpret_cast<const double*>(scratch.host);
+    auto scatter_direct = [&](auto* pm) {
+      const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(host_threads(), rows >> 15));
+      host_parallel(parts, [&](int k) {
+        for (int64_t i = rows * k / parts, e = rows * (k + 1) / parts; i < e; ++i) y[(int64_t)pm[row0 + i]] = t[i];
+      });
+    };
+    if (perm_code == HB_I32) scatter_direct(reinterpret_cast<const int32_t*>(perm));
+    else scatter_direct(reinterpret_cast<const int64_t*>(perm));
     return HB_OK;
   }
   // un-permute on the host straight from the pinned stage: y[perm[row0 + i]] = row sum i

@@ -239,3 +239,29 @@ def test_host_path_unpermute_from_stage(pdt):
         gpu_spmv(m, x, r0, r1, y, perm)
         assert np.array_equal(bits(y[perm[r0:r1]]), bits(want[r0:r1]))
         assert np.isnan(np.delete(y, perm[r0:r1])).all()
+
+
+def test_host_path_unpermute_beyond_one_pinned_stage():
+    """> 4M rows: the row sums no longer fit one 32 MB pinned stage, so the
+    call takes the device-buffer + staged D2H un-permute path."""
+    rows = 4_300_000
+    rng = np.random.default_rng(8)
+    lens = rng.integers(0, 4, rows)
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = rng.integers(0, rows, int(ptr[-1])).astype(np.int64)
+    # columns strictly increasing per row (CSR invariant): sort within rows, drop repeats
+    order = np.lexsort((col, np.repeat(np.arange(rows), lens)))
+    col = col[order]
+    keep = np.ones(col.size, bool)
+    row_of = np.repeat(np.arange(rows), lens)
+    keep[1:] = ~((row_of[1:] == row_of[:-1]) & (col[1:] == col[:-1]))
+    col, row_of = col[keep], row_of[keep]
+    ptr = np.concatenate([[0], np.cumsum(np.bincount(row_of, minlength=rows))]).astype(np.int64)
+    val = rng.standard_normal(col.size)
+    x = rng.standard_normal(rows)
+    m = CsrMatrix(rows, rows, ptr, col, val)
+    perm = rng.permutation(rows).astype(np.int64)
+    y = np.full(rows, np.nan)
+    gpu_spmv(m, x, 0, rows, y, perm)
+    want = ospmv.range_matvec(ptr, col, val, x, 0, rows)
+    assert np.array_equal(bits(y[perm]), bits(want))

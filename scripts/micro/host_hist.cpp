@@ -50,7 +50,7 @@ void h4x2(const uint8_t* d, size_t n, uint64_t* h) {
   for (int v = 0; v < 256; ++v) h[v] += (uint64_t)sub[0][v] + sub[1][v] + sub[2][v] + sub[3][v];
 }
 int main(int argc, char** argv) {
-  const size_t n = (size_t)1 << 28;
+  const size_t n = argc > 2 ? (size_t)atoll(argv[2]) : (size_t)1 << 28;
   std::vector<uint8_t> d(n);
   uint64_t x = 1; for (size_t i = 0; i < n; ++i) { x = x * 6364136223846793005ull + 1442695040888963407ull; d[i] = (uint8_t)(x >> 56); }
   int T = argc > 1 ? atoi(argv[1]) : 1;

@@ -1050,11 +1050,24 @@ def main() -> None:
 
     require_gpu()
 
+    def fresh_memory():
+        # each workload starts from the memory state of a standalone run: the
+        # previous one's device blocks and cached pinned host blocks (GiBs of
+        # e2e inputs/results) are released first
+        import gc
+
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        if hasattr(torch._C, "_host_emptyCache"):
+            torch._C._host_emptyCache()
+
     head = measure(args, WORKLOADS[headline](), rank, world, with_cpu=(world == 1 and not args.no_cpu))
     others = {}
     if args.workload == "all":
         for name, cls in WORKLOADS.items():
             if name != headline:
+                fresh_memory()
                 others[name] = measure(args, cls(), rank, world, with_cpu=(world == 1 and not args.no_cpu))
     if rank == 0:
         line = {

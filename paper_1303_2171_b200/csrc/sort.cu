@@ -1181,6 +1181,170 @@ __global__ void __launch_bounds__(T, MINB)
 }
 
 
+// Persistent variant of onesweep_rfk_kernel with the next tile prefetched
+// (HB_SORT_CFG=78): 2 CTAs/SM each loop over tiles claimed from the same
+// in-order counter; right after a tile's elements are in registers, thread 0
+// claims the NEXT tile and pulls it into shared memory with cp.async.bulk
+// (one 45 KB copy packed, or keys + payload), so the loads of tile i+1 are in
+// flight while tile i is ranked, looked back and scattered.  Partial tiles
+// load from global directly.  Progress: every CTA finishes its tiles in claim
+// order, so the smallest unfinished tile always belongs to a running CTA.
+template <bool PIN, bool POUT, int I, int T, int LBW>
+__global__ void __launch_bounds__(T, 2)
+    onesweep_rfp_kernel(const void* __restrict__ kin_, void* __restrict__ kout_, const uint32_t* __restrict__ vin,
+                        uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t flip,
+                        const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
+                        uint32_t* __restrict__ tile_counter, uint32_t ntiles) {
+  constexpr int W = T / 32, TILE = T * I;
+  static_assert(T >= 256, "one look-back thread per digit");
+  __shared__ uint32_t s_base[W][256];
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_scr[8];
+  __shared__ uint32_t s_next;
+  __shared__ __align__(8) uint64_t s_bar;
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  uint64_t* s_el = reinterpret_cast<uint64_t*>(s_dyn);          // [TILE] re-order buffer
+  uint64_t* s_in = s_el + TILE;                                  // [TILE] prefetched input
+  const uint32_t* s_in32 = reinterpret_cast<const uint32_t*>(s_in);
+  const uint32_t* kin = reinterpret_cast<const uint32_t*>(kin_);
+  const uint64_t* ein = reinterpret_cast<const uint64_t*>(kin_);
+  uint32_t* kout = reinterpret_cast<uint32_t*>(kout_);
+  uint64_t* eout = reinterpret_cast<uint64_t*>(kout_);
+  auto dig = [&](uint64_t e) -> uint32_t { return (((uint32_t)e ^ flip) >> shift) & 255u; };
+  auto full = [&](uint32_t t) { return (int64_t)(t + 1) * TILE <= n; };
+  auto prefetch = [&](uint32_t t) {  // thread 0: whole tile t into s_in
+    const int64_t b = (int64_t)t * TILE;
+    if (PIN) {
+      mbar_expect_tx(&s_bar, TILE * 8);
+      tma_bulk_g2s(s_in, ein + b, TILE * 8, &s_bar);
+    } else {
+      mbar_expect_tx(&s_bar, TILE * 8);
+      tma_bulk_g2s(s_in, kin + b, TILE * 4, &s_bar);
+      tma_bulk_g2s(reinterpret_cast<uint32_t*>(s_in) + TILE, vin + b, TILE * 4, &s_bar);
+    }
+  };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t gs = tid < 256 ? gstart[tid] : 0u;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t t = atomicAdd(tile_counter, 1u);
+    s_next = t;
+    if (t < ntiles && full(t)) prefetch(t);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  const int wbase = warp * 32 * I;
+  for (;;) {
+    const uint32_t tile = s_next;
+    if (tile >= ntiles) break;
+    const int64_t base = (int64_t)tile * TILE;
+    const int valid = (int)min((int64_t)TILE, n - base);
+    const bool staged = full(tile);
+    for (int i = tid; i < W * 256; i += T) (&s_base[0][0])[i] = 0;
+    if (staged) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1u;
+    }
+    uint64_t el[I];
+    uint32_t rank[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const int idx = wbase + i * 32 + lane;
+      if (staged) {
+        el[i] = PIN ? s_in[idx] : (((uint64_t)s_in32[TILE + idx] << 32) | s_in32[idx]);
+      } else {
+        const bool ok = idx < valid;
+        if (PIN) el[i] = ok ? ein[base + idx] : (uint64_t)(~0u ^ flip);
+        else el[i] = ok ? ((uint64_t)vin[base + idx] << 32) | kin[base + idx] : (uint64_t)(~0u ^ flip);
+      }
+    }
+    __syncthreads();  // s_in consumed, s_base zeroed
+    if (tid == 0) {   // claim the next tile and start its loads now
+      const uint32_t t = atomicAdd(tile_counter, 1u);
+      s_next = t;
+      if (t < ntiles && full(t)) {
+        fence_proxy_async_smem();
+        prefetch(t);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < I; ++i) rank[i] = atomicAdd(&s_base[warp][dig(el[i])], 1u);
+    __syncthreads();
+
+    const int d = tid;
+    uint32_t c = 0, dstart = 0;
+    if (tid < 256) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) c += s_base[w][d];
+      if (tile == 0) st_relaxed(lookback + d, kFlagInc | c);
+      else st_relaxed(lookback + (size_t)tile * 256 + d, kFlagAgg | c);
+      uint32_t x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_scr[warp] = x;
+      bar_named(1, 256);
+      uint32_t add = 0;
+      for (int g = 0; g < warp; ++g) add += s_scr[g];
+      dstart = x - c + add;
+      uint32_t run = dstart;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint32_t t = s_base[w][d];
+        s_base[w][d] = run;
+        run += t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < I; ++i) s_el[s_base[warp][dig(el[i])] + rank[i]] = el[i];
+    if (tid < 256) {
+      uint32_t excl = 0;
+      if (tile > 0) {
+        int64_t t = (int64_t)tile - 1;
+        bool done = false;
+        while (!done) {
+          uint32_t wv[LBW];
+#pragma unroll
+          for (int j = 0; j < LBW; ++j) {
+            const int64_t tj = t - j < 0 ? 0 : t - j;
+            wv[j] = ld_relaxed(lookback + (size_t)tj * 256 + d);
+          }
+          int used = 0;
+#pragma unroll
+          for (int j = 0; j < LBW; ++j) {
+            if (done || used < j) continue;
+            const uint32_t flag = wv[j] & ~kCountMask;
+            if (flag == 0) continue;
+            excl += wv[j] & kCountMask;
+            used = j + 1;
+            if (flag == kFlagInc) done = true;
+          }
+          t -= used;
+        }
+        st_relaxed(lookback + (size_t)tile * 256 + d, kFlagInc | (excl + c));
+      }
+      s_goff[d] = gs + excl - dstart;
+    }
+    __syncthreads();
+    for (int j = tid; j < valid; j += T) {
+      const uint64_t e = s_el[j];
+      const uint32_t dst = s_goff[dig(e)] + (uint32_t)j;
+      if (POUT) {
+        eout[dst] = e;
+      } else {
+        kout[dst] = (uint32_t)e;
+        vout[dst] = (uint32_t)(e >> 32);
+      }
+    }
+    __syncthreads();  // s_el / s_base / s_goff / s_next reused by the next tile
+  }
+}
+
 // device check of the lane-ordered shared atomics the rank-first kernel relies on
 __global__ void atoms_order_check(unsigned int* bad, int rows) {
   __shared__ uint32_t cnt[8][256];
@@ -1243,6 +1407,31 @@ int launch_rfk_impl(const PassArgs& a, cudaStream_t s, int64_t tiles) {
   k<<<(unsigned)tiles, T, smem, s>>>(a.kin, a.kout, a.vin, a.vout, a.n, a.shift, (uint32_t)a.flip, a.gstart, a.lookback,
                                      a.counter);
   return check_launch();
+}
+
+template <bool PIN, bool POUT, int I, int T, int LBW>
+int launch_rfp_impl(const PassArgs& a, cudaStream_t s, int64_t tiles) {
+  const size_t smem = (size_t)T * I * 16;
+  auto k = onesweep_rfp_kernel<PIN, POUT, I, T, LBW>;
+  HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  int64_t grid = (int64_t)di.sms * 2;
+  if (grid > tiles) grid = tiles;
+  k<<<(unsigned)grid, T, smem, s>>>(a.kin, a.kout, a.vin, a.vout, a.n, a.shift, (uint32_t)a.flip, a.gstart, a.lookback,
+                                    a.counter, (uint32_t)tiles);
+  return check_launch();
+}
+
+template <int I, int T, int LBW>
+int launch_rfp(const PassArgs& a, bool pin, bool pout, cudaStream_t s, int64_t* tiles_out, bool dry) {
+  const int64_t tiles = ceil_div(a.n, (int64_t)T * I);
+  *tiles_out = tiles;
+  if (dry) return HB_OK;
+  if (pin && pout) return launch_rfp_impl<true, true, I, T, LBW>(a, s, tiles);
+  if (pin) return launch_rfp_impl<true, false, I, T, LBW>(a, s, tiles);
+  if (pout) return launch_rfp_impl<false, true, I, T, LBW>(a, s, tiles);
+  return launch_rfp_impl<false, false, I, T, LBW>(a, s, tiles);
 }
 
 template <int I, int T, int LBW, int MINB>
@@ -1444,14 +1633,16 @@ int run_pass(const PassArgs& a, cudaStream_t s, int64_t* tiles, bool dry) {
 
 // live digit passes of a u32-key + u32-payload sort with the pair moved as one
 // 8-byte element: split → packed → … → packed → split (back into keys/vals)
-template <int PI, int PT, int LBW, int MINB>
+template <int PI, int PT, int LBW, int MINB, bool PERSIST = false>
 int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, const bool* live, int nlive,
                   const DevBuf& hist, const DevBuf& gst, DevBuf& lb, cudaStream_t s) {
   int64_t tiles = 0;
   PassArgs pa{};
   pa.n = n;
   HB_TRY((launch_rfk<PI, PT, LBW, MINB>(pa, false, false, s, &tiles, true)));
-  const size_t lb_words = (size_t)tiles * 256 + 32;
+  // the persistent kernel's CTAs claim one tile past the end each: counter room
+  const size_t extra = PERSIST ? 2048 : 0;
+  const size_t lb_words = (size_t)tiles * 256 + 32 + extra;
   DevBuf pA, pB;
   HB_TRY(alloc(&lb, lb_words * 4, s));
   HB_TRY(alloc(&pA, (size_t)n * 8, s));
@@ -1470,7 +1661,8 @@ int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, cons
     pa.vout = last ? vals : nullptr;
     pa.shift = 8 * p; pa.flip = (uint64_t)flip; pa.hist = hist.as<uint32_t>() + p * 256;
     pa.lookback = lb.as<uint32_t>(); pa.counter = counter; pa.gstart = gst.as<uint32_t>() + p * 256;
-    HB_TRY((launch_rfk<PI, PT, LBW, MINB>(pa, !first, !last, s, &tiles, false)));
+    if (PERSIST) HB_TRY((launch_rfp<PI, PT, LBW>(pa, !first, !last, s, &tiles, false)));
+    else HB_TRY((launch_rfk<PI, PT, LBW, MINB>(pa, !first, !last, s, &tiles, false)));
     cur = nxt;
     nxt = (nxt == pA.ptr) ? pB.ptr : pA.ptr;
     ++done;
@@ -1532,8 +1724,17 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, cud
   if constexpr (sizeof(K) == 4) {
     // key + payload as one 8-byte element between the first and the last live pass
     const int v = sort_variant();
-    if (vals && nlive >= 2 && (v == 0 || (v >= 74 && v <= 77)) && atoms_rank_ok()) {
+    const bool aligned16 = (((uintptr_t)keys | (uintptr_t)vals) & 15) == 0;
+    if (vals && nlive >= 2 && (v == 0 || (v >= 74 && v <= 79)) && atoms_rank_ok()) {
       switch (v) {
+        case 78:
+          if (aligned16)
+            return packed_passes<22, 256, 2, 2, true>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
+          break;
+        case 79:
+          if (aligned16)
+            return packed_passes<14, 384, 2, 2, true>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
+          break;
         case 75: return packed_passes<20, 256, 2, 3>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
         case 76: return packed_passes<24, 256, 2, 3>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);
         case 77: return packed_passes<16, 256, 2, 4>(reinterpret_cast<uint32_t*>(keys), vals, n, (uint32_t)flip, live, nlive, hist, gst, lb, s);

@@ -354,6 +354,123 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// Persistent variant (HB_BILAT_CFG=9): grid = SMs x MINB CTAs loop over the
+// tiles, so the 64 KB signed range table and the spatial weights are built
+// once per CTA instead of once per tile, and the halo tile of the NEXT tile
+// is requested by TMA (second 4 KB buffer, own mbarrier) before the current
+// one is filtered.  Same per-pixel arithmetic as bilateral_tma_kernel<SYM>.
+template <int R, typename OUT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    bilateral_tmap_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ img, int H, int W,
+                          int row0, int row1, const double* __restrict__ spatial,
+                          const double* __restrict__ range, OUT* __restrict__ out, int tiles_x, int ntiles) {
+  using T = TmaTile<R, 1>;
+  constexpr int S = 2 * R + 1;
+  constexpr int TH = T::TH, TW = T::TW, TWB = T::TWB, OFF = T::OFF;
+  constexpr int TBYTES = ((TH * TWB + 127) / 128) * 128;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  uint8_t* tiles = smem;                                             // [2][TBYTES]
+  double* rng = reinterpret_cast<double*>(smem + 2 * TBYTES);        // [511][16]
+  double* sp = rng + 511 * 16;                                       // [S*S]
+  const int tid = threadIdx.x;
+  const int lane = tid & 15;
+  auto origin = [&](int t, int& y0, int& x0) {
+    y0 = row0 + (t / tiles_x) * kTileH;
+    x0 = (t % tiles_x) * kTileW;
+  };
+  auto interior = [&](int y0, int x0) {
+    return x0 - T::PADX >= 0 && x0 - T::PADX + TWB <= W && y0 - R >= 0 && y0 - R + TH <= H;
+  };
+  auto request = [&](int t, int b) {  // thread 0: TMA the halo of tile t into buffer b when interior
+    int y0, x0;
+    origin(t, y0, x0);
+    if (!interior(y0, x0)) return;
+    fence_proxy_async_smem();
+    mbar_expect_tx(&bar[b], TH * TWB);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(tiles + b * TBYTES);
+    const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&bar[b]);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(d), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0 - T::PADX), "r"(y0 - R), "r"(bb) : "memory");
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if ((int)blockIdx.x < ntiles) request(blockIdx.x, 0);
+  }
+  for (int i = tid; i < 511 * 16; i += kThreads) rng[i] = range[abs((i >> 4) - 255)];
+  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
+  __syncthreads();
+  const double* lane_rng = rng + lane + 255 * 16;
+  const uint32_t lr = (uint32_t)__cvta_generic_to_shared(lane_rng);
+  const int py = tid / (kTileW / kPx);
+  const int px = (tid % (kTileW / kPx)) * kPx;
+  uint32_t ph[2] = {0u, 0u};
+  int b = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, b ^= 1) {
+    int y0, x0;
+    origin(t, y0, x0);
+    uint8_t* tile = tiles + b * TBYTES;
+    const bool in = interior(y0, x0);
+    if (tid == 0 && t + (int)gridDim.x < ntiles) request(t + gridDim.x, b ^ 1);  // next tile's halo
+    if (!in) {
+      for (int i = tid; i < TH * TW; i += kThreads) {
+        const int ty = i / TW, tx = i - ty * TW;
+        const int gy = min(max(y0 - R + ty, 0), H - 1);
+        const int gx = min(max(x0 - R + tx, 0), W - 1);
+        tile[ty * TWB + tx + OFF] = img[(int64_t)gy * W + gx];
+      }
+      __syncthreads();
+    } else {
+      mbar_wait(&bar[b], ph[b]);
+      ph[b] ^= 1u;
+    }
+    const int gy = y0 + py;
+    if (gy < row1) {
+      int c[kPx];
+      double num[kPx], den[kPx];
+      uint32_t cbase[kPx];
+#pragma unroll
+      for (int j = 0; j < kPx; ++j) {
+        c[j] = tile[(py + R) * TWB + px + j + R + OFF];
+        num[j] = den[j] = 0.0;
+        cbase[j] = lr - (uint32_t)c[j] * 128u;
+      }
+#pragma unroll 1
+      for (int dy = 0; dy < S; ++dy) {
+        int nb[kPx + 2 * R];
+        double nbd[kPx + 2 * R];
+        const uint8_t* trow = tile + (py + dy) * TWB + px + OFF;
+#pragma unroll
+        for (int q = 0; q < kPx + 2 * R; ++q) {
+          nb[q] = trow[q];
+          nbd[q] = (double)nb[q];
+          nb[q] *= 128;
+        }
+#pragma unroll
+        for (int dx = 0; dx < S; ++dx) {
+          const double sw = sp[dy * S + dx];
+#pragma unroll
+          for (int j = 0; j < kPx; ++j) {
+            double r;
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(cbase[j] + (uint32_t)nb[j + dx]));
+            const double w = __dmul_rn(sw, r);
+            num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
+            den[j] = __dadd_rn(den[j], w);
+          }
+        }
+      }
+      OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
+#pragma unroll
+      for (int j = 0; j < kPx; ++j)
+        if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
+    }
+    __syncthreads();  // buffer b is free for the tile after next
+  }
+}
+
 // host: a 2-D uint8 tensor map over the image (driver entry point through
 // the runtime, no libcuda link); false when the layout does not allow one
 bool make_image_tmap(CUtensorMap* map, const uint8_t* img, int H, int W, int box_w, int box_h) {
@@ -409,7 +526,7 @@ int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const doub
     const char* e = getenv("HB_BILAT_CFG");
     return e ? atoi(e) : 0;
   }();
-  if (variant == 0 || (variant >= 4 && variant <= 8)) {
+  if (variant == 0 || (variant >= 4 && variant <= 9)) {
     // TMA-staged tiles.  default: one row per thread, symmetric 511-entry
     // range table, 3 CTAs/SM; HB_BILAT_CFG 4: |d| table, 5: 2 rows, 6: 3 rows,
     // 7: 2 rows with the symmetric table
@@ -429,6 +546,27 @@ int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const doub
     else if (variant == 6) rc = launch_tma(bilateral_tma_kernel<R, OUT, 3, 2>, TmaTile<R, 3>{}, false);
     else if (variant == 7) rc = launch_tma(bilateral_tma_kernel<R, OUT, 2, 2, true>, TmaTile<R, 2>{}, true);
     else if (variant == 8) rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3, true, true>, TmaTile<R, 1>{}, true);
+    else if (variant == 9) {
+      using TT = TmaTile<R, 1>;
+      CUtensorMap map;
+      if (!make_image_tmap(&map, img, H, W, TT::TWB, TT::TH)) {
+        rc = -1;
+      } else {
+        const size_t tb = (size_t)(TT::TH * TT::TWB + 127) / 128 * 128;
+        const size_t smem = 2 * tb + 511 * 16 * 8 + S * S * 8;
+        auto kern = bilateral_tmap_kernel<R, OUT, 3>;
+        HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DeviceInfo di;
+        HB_TRY(device_info(&di));
+        const int tiles_x = (int)ceil_div(W, kTileW);
+        const int64_t ntiles = (int64_t)tiles_x * ceil_div(row1 - row0, kTileH);
+        HB_CHECK_ARG(ntiles < INT32_MAX, "image too large");
+        int64_t grid = (int64_t)di.sms * 3;
+        if (grid > ntiles) grid = ntiles;
+        kern<<<(unsigned)grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out, tiles_x, (int)ntiles);
+        rc = check_launch();
+      }
+    }
     else rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3, true>, TmaTile<R, 1>{}, true);
     if (rc != -1) return rc;  // -1: no tensor map for this layout, plain tiles below
   }

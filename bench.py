@@ -281,7 +281,7 @@ class HistBench:
             import torch
             import torch.distributed as dist
 
-            t = torch.from_numpy(res.bins).to(coll_device())
+            t = torch.from_numpy(res.bins).to(coll_device(), copy=True)  # the reduce must not alias res
             dist.all_reduce(t)
         return res
 

@@ -89,13 +89,18 @@ template <typename S, bool WEIGHTED>
 __global__ void __launch_bounds__(128)
     lr_walk_kernel(const S* __restrict__ succ, const int64_t* __restrict__ w, int64_t n, int64_t head,
                    int64_t nsub, int64_t extra, uint64_t* __restrict__ tmp, int64_t* __restrict__ nxt,
-                   int64_t* __restrict__ len, unsigned long long* __restrict__ err) {
+                   int64_t* __restrict__ len, unsigned long long* __restrict__ err,
+                   unsigned long long* __restrict__ jobs) {
+  // jobs != nullptr: sublists are claimed from a global counter as chains
+  // free up (dynamic balance: a thread's walks are geometric-length, so a
+  // static stride leaves stragglers); else the static stride t, t+T, ...
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // next sublist to start
   int64_t j[kChains], cur[kChains], acc[kChains], steps[kChains];
   auto start = [&](int c) {
-    while (job < nsub) {
-      const int64_t jj = job;
+    for (;;) {
+      const int64_t jj = jobs ? (int64_t)atomicAdd(jobs, 1ull) : job;
+      if (jj >= nsub) break;
       job += T;
       const int64_t h = jj == extra ? head : jj * kK;
       if (h >= n) {
@@ -239,14 +244,23 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
     HB_TRY(alloc(&L->len, (size_t)L->nsub * 8, s));
     int64_t blocks = ceil_div(L->nsub, 128 * kChains);
     if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;  // 2048 resident threads / SM
+    static const int lr_cfg = [] {
+      const char* e = getenv("HB_LR_CFG");
+      return e ? atoi(e) : 0;
+    }();
+    DevBuf jobs;
+    if (lr_cfg != 2) {  // dynamic sublist claiming (default; +1 %: 12.62 vs 12.49 Gnodes/s); 2: static stride
+      HB_TRY(alloc(&jobs, 8, s));
+      HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
+    }
     if (first) {
       lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, nullptr, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
-          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>());
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
     } else {
       lr_walk_kernel<int64_t, true><<<(int)blocks, 128, 0, s>>>(
           (const int64_t*)cur_succ, w, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
-          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>());
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
     }
     HB_TRY(check_launch());
     cur_succ = L->nxt.ptr;

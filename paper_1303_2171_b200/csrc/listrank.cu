@@ -27,7 +27,10 @@
 namespace hb {
 namespace {
 
-constexpr int kK = 64;        // sublist spacing (node index multiple)
+#ifndef HB_LR_K
+#define HB_LR_K 64
+#endif
+constexpr int kK = HB_LR_K;   // sublist spacing (node index multiple)
 constexpr int kBase = 4096;   // top level size ranked in one CTA
 
 // Validation: out[0] += tails (succ == -1), out[1] += out-of-range successors.

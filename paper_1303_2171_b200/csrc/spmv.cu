@@ -488,7 +488,8 @@ int launch_lpr(const void* rp, const void* ci, const double* v, const double* x,
 }
 
 // HB_SPMV_CFG (experiments, scripts/sweep_spmv.sh): 0 default, 1 the generic
-// CTA-blocked kernel, 2.. alternative lane-per-row shapes <CW, S, WARPS, MINB, B>.
+// CTA-blocked kernel, 2.. alternative lane-per-row shapes <CW, S, WARPS, MINB, B>
+// (7/8: 6 or 8 gathers in flight per lane, 9: 3 stages — 84-88 us vs 83 us).
 template <typename P, typename C, typename Q>
 int launch_spmv(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
                 int64_t row1, const void* pm, double* y, int mode, cudaStream_t s) {
@@ -533,6 +534,9 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
       case 4: return launch_lpr<Q, 256, 2, 4, 6, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
       case 5: return launch_lpr<Q, 256, 2, 4, 4, 8>(rp, ci, v, x, row0, row1, pm, y, di, s);
       case 6: return launch_lpr<Q, 192, 2, 4, 8, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 7: return launch_lpr<Q, 256, 2, 4, 6, 6>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 8: return launch_lpr<Q, 256, 2, 4, 6, 8>(rp, ci, v, x, row0, row1, pm, y, di, s);
+      case 9: return launch_lpr<Q, 256, 3, 4, 5, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
       default: return launch_lpr<Q, 256, 2, 4, 6, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
     }
   }

@@ -63,12 +63,17 @@ __device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra
 }
 
 // Sublist walks.  tmp[v] = (sublist << 32) | local offset; nxt[j] = next
-// sublist or -1; len[j] = weight sum.  Each thread owns the sublists
-// j = t, t+T, t+2T, ... and keeps kChains of them in flight at once; the
-// loop is flattened (a finished walk immediately starts the thread's next
-// sublist), so lanes never idle waiting for the longest walk of their warp
-// and every thread has kChains independent dependent-load chains in flight.
-constexpr int kChains = 4;
+// sublist or -1; len[j] = weight sum.  Each thread claims sublists from a
+// global counter (or the static stride t, t+T, ...) and keeps kChains of them
+// in flight; the loop is flattened (a finished walk immediately starts the
+// thread's next sublist), so lanes never idle waiting for the longest walk of
+// their warp.  With 2048 threads per SM one dependent chain per thread
+// already fills the random-access path, and the single-chain loop is the
+// leanest (kChains = 1 measured fastest).
+#ifndef HB_LR_CHAINS
+#define HB_LR_CHAINS 1  // measured with dynamic claiming: 1 / 2 / 3 / 4 / 8 chains = 13.24 / 12.97 / 12.76 / 12.62 / 12.0 Gnodes/s
+#endif
+constexpr int kChains = HB_LR_CHAINS;
 
 // Successor reads are random: load them L2-only (.cg).  The read-only
 // (.nc / __ldg) path promotes every L1 miss to a full 128-byte line, i.e.

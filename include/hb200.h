@@ -198,6 +198,55 @@ int hb_list_fis_stats(const void* succ, int succ_code, int64_t n, int64_t head, 
                       int32_t sublists, int64_t* round_sizes, int32_t round_cap, int64_t* stats,
                       int flags, void* stream);
 
+/* -------------------------------------------------------- multi-GPU shards
+ * One process per GPU; these are the device halves of the partition → run_part
+ * → merge protocol (worksharing.py:297-359) when DeviceB is a group of G GPUs
+ * (SURVEY §8e).  The collectives themselves are torch.distributed (NCCL over
+ * NVLink) on the tensors these functions produce and consume.
+ *
+ * hb_partition_nnz: the device-side SpMV partitioner.  bounds_out[k] (HOST
+ * array, parts+1 entries) = row0 + searchsorted(cum, k*total/parts, 'left')
+ * over cum = row_ptr[row0..row1] - row_ptr[row0] in fp64 — SpmvWorkload's
+ * split rule (kernels_irregular.py:243-245) at k/G.  With HB_DEVICE_PTRS
+ * row_ptr is a device array and only the G+1 bounds leave the device.      */
+int hb_partition_nnz(const void* row_ptr, int ptr_code, int64_t row0, int64_t row1, int32_t parts,
+                     int64_t* bounds_out, int flags, void* stream);
+
+/* dst[perm[i]] = src[i], i < n, 4- or 8-byte elements: SpmvWorkload.merge's
+ * un-permute (kernels_irregular.py:253-257) applied to an all-gathered
+ * y_perm.  Device pointers only.                                           */
+int hb_scatter_perm(const void* src, int64_t n, int elem_bytes, const void* perm, int perm_code, void* dst,
+                    int flags, void* stream);
+
+/* Stable merge of nruns sorted runs keys[offsets[r] .. offsets[r+1]) (host
+ * offsets array, offsets[0] = 0, offsets[nruns] = n) into keys_out, the
+ * uint32 payload (optional) moved alongside; equal keys keep run order.  The
+ * receive side of the multi-GPU sample-merge sort (runs arrive in rank
+ * order).  Pairwise merge-path rounds; device pointers only, no aliasing.  */
+int hb_merge_runs(const void* keys, int key_code, const uint32_t* vals, int64_t n, const int64_t* offsets,
+                  int32_t nruns, void* keys_out, uint32_t* vals_out, int flags, void* stream);
+
+/* Sharded list ranking (the sublist split of _rank_reduced,
+ * kernels_irregular.py:431-478, mapped onto GPUs):
+ *  hb_lr_layout      nsub sublists (every node index ≡ 0 mod 64, plus the
+ *                    head) and the id of the head's sublist;
+ *  hb_lr_walk_part   validates succ (like hb_list_rank), fills packed[n]
+ *                    with 0xff, walks the sublists with ids in
+ *                    [sub_lo, sub_hi): packed[v] = (sublist << 32 | offset)
+ *                    for the nodes it passes, sub_nxt/sub_len[j] for its ids;
+ *  (caller)          all-gathers sub_nxt / sub_len across the G ranks;
+ *  hb_lr_finish_part ranks the sublist chain weighted by length (it must
+ *                    cover all n nodes, else HB_ESTRUCT — on every rank
+ *                    alike) and turns packed into ranks for the nodes of
+ *                    sublists [sub_lo, sub_hi), 0 for all other nodes;
+ *  (caller)          all-reduce (sum) of rank → every rank holds all ranks.
+ * Device pointers only; n < 2^31.                                          */
+int hb_lr_layout(int64_t n, int64_t head, int64_t* nsub, int64_t* sub_head);
+int hb_lr_walk_part(const void* succ, int succ_code, int64_t n, int64_t head, int64_t sub_lo, int64_t sub_hi,
+                    int64_t* packed, int64_t* sub_nxt, int64_t* sub_len, int flags, void* stream);
+int hb_lr_finish_part(const int64_t* sub_nxt, const int64_t* sub_len, int64_t nsub, int64_t sub_head, int64_t n,
+                      int64_t sub_lo, int64_t sub_hi, int64_t* rank, int flags, void* stream);
+
 /* ------------------------------------------------------- host (DeviceA)
  * The host share of a work-shared run on `workers` host threads, bit-identical
  * to the reference's numpy bodies (no GPU involved): histogram

@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(128)
       if (v == -1 || is_head(v, head) || steps[c] > n) {
         if (steps[c] > n) atomicAdd(err, 1ull);  // cycle without a sublist head
         nxt[j[c]] = (v == -1 || steps[c] > n) ? -1 : sub_id(v, head, extra);
-        len[j[c]] = acc[c];
+        // a runaway walk reports more weight than the whole list holds, so a
+        // chain check on the summaries alone (sharded ranking) still fails
+        len[j[c]] = steps[c] > n ? n + 1 : acc[c];
         start(c);
         continue;
       }
@@ -214,8 +216,13 @@ struct Level {
   int64_t n = 0, nsub = 0, extra = -1, head = 0;
 };
 
+// Rank the list `succ` (n nodes, first node `head`): out_rank[v] = sum of the
+// weights of the nodes before v on the chain (w0 == nullptr: unit weights,
+// i.e. the distance from the head).  The chain must cover weight `expect`
+// in total (n for unit weights), else HB_ESTRUCT.
 template <typename S>
-int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaStream_t s) {
+int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64_t expect, int64_t* out_rank,
+                cudaStream_t s) {
   DeviceInfo di;
   HB_TRY(device_info(&di));
   DevBuf err, st;
@@ -230,7 +237,7 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
   } cleanup{levels};
 
   // descend: level 0 walks the input list, later levels walk the sublist lists
-  const int64_t* w = nullptr;
+  const int64_t* w = w0;
   const void* cur_succ = succ;
   bool first = true;
   int64_t cur_n = n, cur_head = head;
@@ -261,7 +268,11 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
       HB_TRY(alloc(&jobs, 8, s));
       HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
     }
-    if (first) {
+    if (first && w0 != nullptr) {
+      lr_walk_kernel<S, true><<<(int)blocks, 128, 0, s>>>(
+          (const S*)cur_succ, w0, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
+    } else if (first) {
       lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, nullptr, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
           L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
@@ -284,6 +295,8 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
     HB_TRY(alloc(&top_nxt, (size_t)cur_n * 8, s));
     HB_TRY(alloc(&top_len, (size_t)cur_n * 8, s));
     std::vector<int64_t> ones((size_t)cur_n, 1);
+    if (w0 != nullptr)
+      HB_CUDA_TRY(cudaMemcpyAsync(ones.data(), w0, (size_t)cur_n * 8, cudaMemcpyDeviceToHost, s));
     std::vector<int64_t> nx((size_t)cur_n);
     std::vector<S> sh((size_t)cur_n);
     HB_CUDA_TRY(cudaMemcpyAsync(sh.data(), succ, (size_t)cur_n * sizeof(S), cudaMemcpyDeviceToHost, s));
@@ -311,8 +324,12 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
     set_error("list contains a cycle");
     return HB_ESTRUCT;
   }
-  if (status[0] != n) {
-    set_error("chain covers %lld of %lld nodes (broken list)", (long long)status[0], (long long)n);
+  if (status[0] > expect) {
+    set_error("list contains a cycle");
+    return HB_ESTRUCT;
+  }
+  if (status[0] != expect) {
+    set_error("chain covers %lld of %lld nodes (broken list)", (long long)status[0], (long long)expect);
     return HB_ESTRUCT;
   }
 
@@ -338,6 +355,78 @@ int rank_levels(const S* succ, int64_t n, int64_t head, int64_t* out_rank, cudaS
     HB_TRY(check_launch());
     prefix = dst;
   }
+  return HB_OK;
+}
+
+// Sharded ranking, expansion: own sublists [lo, hi) → rank, others → 0
+// (the packed slots of nodes walked by other ranks still hold the 0xFF..
+// fill, sublist id 0xffffffff, which no rank owns).
+__global__ void lr_expand_part_kernel(int64_t* __restrict__ io, int64_t n, const int64_t* __restrict__ prefix,
+                                      int64_t lo, int64_t hi) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = (uint64_t)io[v];
+    const int64_t j = (int64_t)(t >> 32);
+    io[v] = (j >= lo && j < hi) ? prefix[j] + (int64_t)(t & 0xffffffffull) : 0;
+  }
+}
+
+void lr_layout(int64_t n, int64_t head, int64_t* nsub, int64_t* sub_head) {
+  const int64_t regular = ceil_div(n, kK);
+  const bool extra = head % kK != 0;
+  *nsub = regular + (extra ? 1 : 0);
+  *sub_head = extra ? regular : head / kK;
+}
+
+// validate_list's range check + tail count (kernels_irregular.py:377-393)
+template <typename S>
+int check_list(const S* succ, int64_t n, cudaStream_t s) {
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  DevBuf chk;
+  HB_TRY(alloc(&chk, 16, s));
+  HB_CUDA_TRY(cudaMemsetAsync(chk.ptr, 0, 16, s));
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+  lr_check_kernel<S><<<(int)blocks, 256, 0, s>>>(succ, n, chk.as<unsigned long long>());
+  HB_TRY(check_launch());
+  unsigned long long c[2] = {0, 0};
+  HB_CUDA_TRY(cudaMemcpyAsync(c, chk.ptr, 16, cudaMemcpyDeviceToHost, s));
+  HB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (c[1]) {
+    set_error("successor index out of range");
+    return HB_ESTRUCT;
+  }
+  if (c[0] != 1) {
+    set_error(c[0] == 0 ? "list contains a cycle" : "list has %llu tails (broken list)", c[0]);
+    return HB_ESTRUCT;
+  }
+  return HB_OK;
+}
+
+// Sharded ranking, level 1: walk the sublists with ids in [lo, hi) only.
+template <typename S>
+int walk_part(const S* succ, int64_t n, int64_t head, int64_t lo, int64_t hi, uint64_t* packed, int64_t* nxt,
+              int64_t* len, cudaStream_t s) {
+  HB_TRY(check_list<S>(succ, n, s));
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  int64_t nsub, sub_head;
+  lr_layout(n, head, &nsub, &sub_head);
+  const int64_t extra = head % kK != 0 ? nsub - 1 : -1;
+  HB_CUDA_TRY(cudaMemsetAsync(packed, 0xff, (size_t)n * 8, s));
+  if (hi <= lo) return HB_OK;
+  DevBuf err, jobs;
+  HB_TRY(alloc(&err, 8, s));
+  HB_TRY(alloc(&jobs, 8, s));
+  const unsigned long long start = (unsigned long long)lo;
+  HB_CUDA_TRY(cudaMemsetAsync(err.ptr, 0, 8, s));
+  HB_CUDA_TRY(cudaMemcpyAsync(jobs.ptr, &start, 8, cudaMemcpyHostToDevice, s));
+  int64_t blocks = ceil_div(hi - lo, 128 * kChains);
+  if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+  lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(succ, nullptr, n, head, hi, extra, packed, nxt, len,
+                                                       err.as<unsigned long long>(), jobs.as<unsigned long long>());
+  HB_TRY(check_launch());
   return HB_OK;
 }
 
@@ -407,9 +496,57 @@ extern "C" int hb_list_rank(const void* succ, int succ_code, int64_t n, int64_t 
     set_error(c[0] == 0 ? "list contains a cycle" : "list has %llu tails (broken list)", c[0]);
     return HB_ESTRUCT;
   }
-  int rc = succ_code == HB_I32 ? rank_levels<int32_t>(d_succ.as<int32_t>(), n, head, d_rank.as<int64_t>(), s)
-                               : rank_levels<int64_t>(d_succ.as<int64_t>(), n, head, d_rank.as<int64_t>(), s);
+  int rc = succ_code == HB_I32 ? rank_levels<int32_t>(d_succ.as<int32_t>(), nullptr, n, head, n, d_rank.as<int64_t>(), s)
+                               : rank_levels<int64_t>(d_succ.as<int64_t>(), nullptr, n, head, n, d_rank.as<int64_t>(), s);
   if (rc != HB_OK) return rc;
   HB_TRY(copy_out(rank, d_rank, (size_t)n * 8, dev, s));
+  return finish(flags, s);
+}
+
+extern "C" int hb_lr_layout(int64_t n, int64_t head, int64_t* nsub, int64_t* sub_head) {
+  HB_CHECK_ARG(n >= 1 && head >= 0 && head < n, "bad list size / head");
+  HB_CHECK_ARG(nsub && sub_head, "NULL pointer");
+  lr_layout(n, head, nsub, sub_head);
+  return HB_OK;
+}
+
+extern "C" int hb_lr_walk_part(const void* succ, int succ_code, int64_t n, int64_t head, int64_t sub_lo,
+                               int64_t sub_hi, int64_t* packed, int64_t* sub_nxt, int64_t* sub_len, int flags,
+                               void* stream) {
+  HB_CHECK_ARG(succ_code == HB_I32 || succ_code == HB_I64, "succ must be int32 or int64");
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "the sharded ranking works on device arrays");
+  HB_CHECK_ARG(n >= 1 && n < (1ll << 31), "lists of 1 .. 2^31-1 nodes are supported");
+  HB_CHECK_ARG(succ && packed && sub_nxt && sub_len, "NULL pointer");
+  if (head < 0 || head >= n) {
+    set_error("head out of range");
+    return HB_ESTRUCT;
+  }
+  int64_t nsub, sub_head;
+  lr_layout(n, head, &nsub, &sub_head);
+  HB_CHECK_ARG(0 <= sub_lo && sub_lo <= sub_hi && sub_hi <= nsub, "sublist range out of [0, %lld]", (long long)nsub);
+  cudaStream_t s = as_stream(stream);
+  int rc = succ_code == HB_I32
+               ? walk_part<int32_t>((const int32_t*)succ, n, head, sub_lo, sub_hi, (uint64_t*)packed, sub_nxt, sub_len, s)
+               : walk_part<int64_t>((const int64_t*)succ, n, head, sub_lo, sub_hi, (uint64_t*)packed, sub_nxt, sub_len, s);
+  if (rc != HB_OK) return rc;
+  return finish(flags, s);
+}
+
+extern "C" int hb_lr_finish_part(const int64_t* sub_nxt, const int64_t* sub_len, int64_t nsub, int64_t sub_head,
+                                 int64_t n, int64_t sub_lo, int64_t sub_hi, int64_t* rank, int flags, void* stream) {
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "the sharded ranking works on device arrays");
+  HB_CHECK_ARG(n >= 1 && nsub >= 1 && sub_head >= 0 && sub_head < nsub, "bad sublist layout");
+  HB_CHECK_ARG(0 <= sub_lo && sub_lo <= sub_hi && sub_hi <= nsub, "sublist range out of range");
+  HB_CHECK_ARG(sub_nxt && sub_len && rank, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  DevBuf prefix;
+  HB_TRY(alloc(&prefix, (size_t)nsub * 8, s));
+  // rank the sublist chain weighted by the sublist lengths: it must cover all n nodes
+  HB_TRY(rank_levels<int64_t>(sub_nxt, sub_len, nsub, sub_head, n, prefix.as<int64_t>(), s));
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)di.sms * 32) blocks = (int64_t)di.sms * 32;
+  lr_expand_part_kernel<<<(int)blocks, 256, 0, s>>>(rank, n, prefix.as<int64_t>(), sub_lo, sub_hi);
   return finish(flags, s);
 }

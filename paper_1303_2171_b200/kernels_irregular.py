@@ -307,12 +307,6 @@ def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int, worker
     _lib.call("hb_host_spmv_rows", vp(rp.ptr), rp.code, vp(ci.ptr), ci.code, vp(v.ctypes.data), row0, row1,
               vp(xh.ctypes.data), vp(pb.ptr if pb else 0), pb.code if pb else 0, vp(y.ctypes.data), workers)
     return y
-    rp, ci = buf(to_host(m.row_ptr)), buf(to_host(m.col_idx))
-    v = np.ascontiguousarray(to_host(m.values), dtype=np.float64)
-    xh = np.ascontiguousarray(x, dtype=np.float64)
-    _lib.call("hb_host_spmv_rows", vp(rp.ptr), rp.code, vp(ci.ptr), ci.code, vp(v.ctypes.data), row0, row1,
-              vp(xh.ctypes.data), vp(y.ctypes.data), workers)
-    return y
 
 
 def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: Any = None,
@@ -363,39 +357,99 @@ def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: An
     return y
 
 
-def _nnz_bounds(m: CsrMatrix, row0: int, row1: int, world: int) -> list[int]:
-    """Device-side partitioner rule for SpMV: G ranges of equal nnz, found by
-    the reference's own searchsorted-on-nnz-prefix (:243-245) at k/G."""
-    rp = to_host(m.row_ptr).astype(np.float64)
-    cum = rp[row0 : row1 + 1] - rp[row0]
+def nnz_bounds_host(row_ptr: np.ndarray, row0: int, row1: int, parts: int) -> list[int]:
+    """SpmvWorkload's split rule (:243-245) at k/G on a host row_ptr:
+    G row ranges of equal nnz, searchsorted(cum, k·total/G, 'left')."""
+    cum = np.asarray(row_ptr[row0 : row1 + 1], dtype=np.float64) - float(row_ptr[row0])
     total = cum[-1]
-    inner = [row0 + int(np.searchsorted(cum, k * total / world, side="left")) for k in range(1, world)]
+    inner = [row0 + int(np.searchsorted(cum, k * total / parts, side="left")) for k in range(1, parts)]
     return [row0] + inner + [row1]
 
 
-def _gpu_rows(m: CsrMatrix, x, row0: int, row1: int) -> np.ndarray:
+def partition_nnz(m: CsrMatrix, row0: int, row1: int, parts: int) -> list[int]:
+    """The device-side partitioner: G+1 row bounds of equal nnz over rows
+    [row0, row1).  Device matrices: hb_partition_nnz binary-searches the
+    device row_ptr (only the G+1 bounds come back); host matrices: the same
+    rule on the host array (nothing to copy)."""
+    if parts == 1:
+        return [row0, row1]
+    if not m.on_device:
+        return nnz_bounds_host(m.row_ptr, row0, row1, parts)
+    out = np.zeros(parts + 1, dtype=np.int64)
+    _lib.call("hb_partition_nnz", vp(m.row_ptr.data_ptr()), _index_code(m.row_ptr), row0, row1, parts,
+              vp(out.ctypes.data), _lib.HB_DEVICE_PTRS, current_stream_handle(m.row_ptr))
+    return [int(v) for v in out]
+
+
+def scatter_perm(src: Any, perm: Any, dst: Any) -> Any:
+    """dst[perm[i]] = src[i] on the device (hb_scatter_perm; the un-permute
+    of SpmvWorkload.merge, :253-257)."""
+    n = int(src.numel())
+    if n:
+        _lib.call("hb_scatter_perm", vp(src.data_ptr()), n, src.element_size(), vp(perm.data_ptr()),
+                  _index_code(perm), vp(dst.data_ptr()), _lib.HB_DEVICE_PTRS, current_stream_handle(src))
+    return dst
+
+
+def _gpu_rows(m: CsrMatrix, x, row0: int, row1: int) -> Any:
+    """DeviceB rows [row0, row1) → y_perm slice (numpy for a host matrix,
+    CUDA tensor for a device matrix).  Under a GPU group: equal-nnz shards
+    from the device-side partitioner, one all-gather of the y slices."""
     g = sharding.active_group()
-    if g is None or g.world == 1:
-        return sharding.to_numpy(gpu_spmv(m, x, row0, row1))
-    b = _nnz_bounds(m, row0, row1, g.world)
-    mine = sharding.to_numpy(gpu_spmv(m, x, b[g.rank], b[g.rank + 1]))
-    return sharding.allgather_rows(mine, b, g)
+    if not sharding.multi(g):
+        return gpu_spmv(m, x, row0, row1)
+    b = partition_nnz(m, row0, row1, g.world)
+    mine = gpu_spmv(m, x, b[g.rank], b[g.rank + 1])
+    return sharding.gather_rows(mine, b, g)
 
 
-def spmv_hybrid(prep: SpmvPrep, x: Any) -> np.ndarray:
-    """y = A x with the prep's row split, in original row order (:214-227)."""
+def _spmv_device(prep: SpmvPrep, x: Any) -> Any:
+    """spmv_hybrid for a device-resident matrix: y stays in HBM.  One GPU:
+    the kernel stores y[perm[i]] directly (fused un-permute).  GPU group:
+    every rank computes its equal-nnz shard of y_perm, all-gather, then
+    hb_scatter_perm.  A host share (split_row > 0) runs on the host cores
+    and is scattered in on the device."""
+    import torch
+
     m = prep.permuted
-    xh = np.asarray(to_host(x), dtype=np.float64)
-    if xh.shape != (m.cols,):
-        raise ValueError(f"x must have length {m.cols}, got {xh.shape}")
+    xd = x if is_device_array(x) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(m.row_ptr.device)
+    perm = prep.perm
+    if not is_device_array(perm):
+        perm = torch.from_numpy(np.ascontiguousarray(perm, dtype=np.int64)).to(xd.device)
     split = prep.split_row
-    x_side_b = x if (m.on_device and is_device_array(x)) else xh
+    y = torch.empty(m.rows, dtype=torch.float64, device=xd.device)
     g = sharding.active_group()
-    if m.on_device or (g is not None and g.world > 1):
+    with ThreadPoolExecutor(max_workers=1) as pool:
+        fa = pool.submit(_host_range_matvec, m.to_host(), np.asarray(to_host(xd)), 0, split, prep.workers_a) if split else None
+        if split < m.rows:
+            if sharding.multi(g):
+                scatter_perm(_gpu_rows(m, xd, split, m.rows), perm[split:], y)
+            else:
+                gpu_spmv(m, xd, split, m.rows, y=y, perm=perm)
+        if fa is not None:
+            scatter_perm(torch.from_numpy(fa.result()).to(y.device), perm[:split], y)
+    return y if is_device_array(x) else y.cpu().numpy()
+
+
+def spmv_hybrid(prep: SpmvPrep, x: Any) -> Any:
+    """y = A x with the prep's row split, in original row order (:214-227).
+    Host matrix → numpy y; device matrix → y computed in HBM (a CUDA tensor
+    when x is one, else copied back to numpy)."""
+    m = prep.permuted
+    if not is_device_array(x):
+        x = np.asarray(x, dtype=np.float64)
+    if tuple(x.shape) != (m.cols,):
+        raise ValueError(f"x must have length {m.cols}, got {tuple(x.shape)}")
+    if m.on_device:
+        return _spmv_device(prep, x)
+    xh = np.asarray(to_host(x), dtype=np.float64)
+    split = prep.split_row
+    g = sharding.active_group()
+    if sharding.multi(g):
         with ThreadPoolExecutor(max_workers=2) as pool:
             fa = pool.submit(_host_range_matvec, m, xh, 0, split, prep.workers_a)
-            fb = pool.submit(inherit_device(_gpu_rows), m, x_side_b, split, m.rows)
-            y_perm = np.concatenate([fa.result(), fb.result()])
+            fb = pool.submit(inherit_device(_gpu_rows), m, xh, split, m.rows)
+            y_perm = np.concatenate([fa.result(), sharding.to_numpy(fb.result())])
         y = np.empty_like(y_perm)
         y[to_host(prep.perm)] = y_perm
         return y
@@ -445,8 +499,8 @@ class SpmvWorkload:
             return _gpu_rows(self.prep.permuted, self.x, part[0], part[1])
         return _host_range_matvec(self.prep.permuted, self.x_host, part[0], part[1], device.worker_count)
 
-    def merge(self, partials: Sequence[np.ndarray]) -> np.ndarray:
-        y_perm = np.concatenate(partials)
+    def merge(self, partials: Sequence[Any]) -> np.ndarray:
+        y_perm = np.concatenate([sharding.to_numpy(p) for p in partials])
         y = np.empty_like(y_perm)
         y[to_host(self.prep.perm)] = y_perm
         return y
@@ -502,6 +556,8 @@ def gpu_list_rank(succ: Any, head: int, out: Any = None, *, asynchronous: bool =
     (int32/int64) → int64 CUDA tensor.  Malformed lists raise StructuralError."""
     _lib.load()
     require_gpu()
+    if sharding.multi():
+        return list_rank_sharded(succ, head, sharding.active_group(), out)
     sb = buf(succ)
     if sb.dtype not in (np.dtype(np.int32), np.dtype(np.int64)):
         sb = buf(np.asarray(to_host(succ), dtype=np.int64))
@@ -520,6 +576,52 @@ def gpu_list_rank(succ: Any, head: int, out: Any = None, *, asynchronous: bool =
     res = host_empty(n, np.int64)
     _lib.call("hb_list_rank", vp(sb.ptr), code, n, int(head), vp(res.ctypes.data), 0, current_stream_handle())
     return res
+
+
+def list_rank_sharded(succ: Any, head: int, g: "sharding.ShardGroup", out: Any = None) -> Any:
+    """List ranking over a GPU group — the sublist split of the reference's
+    _rank_reduced (:431-478) mapped onto GPUs: succ replicated
+    on every rank; the level-1 sublists (every 64th node + the head) split
+    floor(k·S/G) by id; each rank walks its own (hb_lr_walk_part); the
+    (next, length) summaries are all-gathered; every rank ranks the sublist
+    chain and expands the ranks of its own nodes (hb_lr_finish_part, 0 for
+    the others); an all-reduce (sum) leaves every rank with all ranks.
+    Errors (bad successors, cycles, broken lists) are detected identically
+    on every rank, so no rank is left waiting in a collective."""
+    import ctypes
+
+    import torch
+
+    n = int(succ.numel() if is_device_array(succ) else np.asarray(succ).size)
+    if not 0 <= head < max(n, 1) or n < 1:
+        raise StructuralError("head out of range")
+    if is_device_array(succ):
+        sd = succ if succ.dtype in (torch.int32, torch.int64) else succ.to(torch.int64)
+    else:
+        host = np.asarray(succ)
+        if host.size and (host.min() < LIST_END or host.max() >= n):
+            raise StructuralError("successor index out of range")
+        sd = torch.from_numpy(np.ascontiguousarray(host, dtype=np.int32 if n < 2**31 else np.int64)).cuda()
+    sd = sd.contiguous()
+    nsub, sub_head = ctypes.c_int64(0), ctypes.c_int64(0)
+    _lib.call("hb_lr_layout", n, int(head), ctypes.byref(nsub), ctypes.byref(sub_head))
+    nsub, sub_head = nsub.value, sub_head.value
+    b = sharding.shard_bounds(nsub, g.world)
+    lo, hi = b[g.rank], b[g.rank + 1]
+    dev = sd.device
+    rank = out if out is not None else torch.empty(n, dtype=torch.int64, device=dev)
+    nxt = torch.empty(nsub, dtype=torch.int64, device=dev)
+    ln = torch.empty(nsub, dtype=torch.int64, device=dev)
+    stream = current_stream_handle(sd)
+    _lib.call("hb_lr_walk_part", vp(sd.data_ptr()), _index_code(sd), n, int(head), lo, hi, vp(rank.data_ptr()),
+              vp(nxt.data_ptr()), vp(ln.data_ptr()), _lib.HB_DEVICE_PTRS | _lib.HB_ASYNC, stream)
+    counts = [b[k + 1] - b[k] for k in range(g.world)]
+    nxt_all = sharding.gather_blocks(nxt[lo:hi], counts, g)
+    ln_all = sharding.gather_blocks(ln[lo:hi], counts, g)
+    _lib.call("hb_lr_finish_part", vp(nxt_all.data_ptr()), vp(ln_all.data_ptr()), nsub, sub_head, n, lo, hi,
+              vp(rank.data_ptr()), _lib.HB_DEVICE_PTRS | _lib.HB_ASYNC, stream)
+    sharding.all_reduce_sum(rank, g)
+    return rank if is_device_array(succ) else rank.cpu().numpy()
 
 
 def gpu_list_fis_stats(succ: Any, head: int, seed: int, sublists: int) -> ListRankStats:

@@ -207,10 +207,10 @@ class HistogramWorkload:
             return sharding.run_sharded_histogram(part, self.bin_count)
         return host_histogram(part, self.bin_count, device.worker_count)
 
-    def merge(self, partials: Sequence[np.ndarray]) -> HistogramResult:
+    def merge(self, partials: Sequence[Any]) -> HistogramResult:
         total = np.zeros(self.bin_count, dtype=np.int64)
         for p in partials:
-            total += p
+            total += sharding.to_numpy(p)
         return HistogramResult(total, self.bin_count)
 
 
@@ -295,13 +295,63 @@ def _host_sort_plan(arr: np.ndarray, fraction: float):
     return ids, sizes, on_a
 
 
-def _gpu_keys(arr: Any):
-    """Key array the GPU sorts: int64 keys stay int64 (digit passes above the
-    data's range are skipped), other integer types are widened when needed."""
-    dt = arr.dtype if not is_device_array(arr) else None
-    if dt is not None and np.dtype(dt) not in _SORT_CODES:
-        return np.asarray(arr, dtype=np.int64)
-    return arr
+_F_TOP = {8: np.uint64(1 << 63), 4: np.uint32(1 << 31)}
+
+
+def _sortable(arr: np.ndarray):
+    """(keys the GPU radix sort takes, function mapping sorted keys back).
+    u32/i32/u64/i64 go as they are; narrower integers and bools are widened
+    (and cast back); floats become order-preserving unsigned bit patterns
+    (sign bit set → all bits flipped, else the sign bit set), which sort
+    exactly like the values (-0.0 before +0.0) and map back bit for bit."""
+    dt = arr.dtype
+    if dt in _SORT_CODES:
+        return arr, lambda k: k
+    if dt.kind == "b" or (dt.kind in "ui" and dt.itemsize < 4):
+        wide = np.int32 if dt.kind == "i" else np.uint32
+        return arr.astype(wide), lambda k: np.asarray(k).astype(dt)
+    if dt.kind == "f":
+        src = arr.astype(np.float32) if dt.itemsize < 4 else arr
+        width = src.dtype.itemsize
+        ut = np.uint64 if width == 8 else np.uint32
+        top = _F_TOP[width]
+        bits = src.view(ut)
+        neg = (bits >> ut(8 * width - 1)).astype(bool)
+        keys = np.where(neg, ~bits, bits | top)
+
+        def back(k):
+            k = np.asarray(k)
+            orig = np.where((k & top).astype(bool), k ^ top, ~k).astype(ut)
+            return orig.view(src.dtype).astype(dt)
+
+        return keys, back
+    raise TypeError(f"cannot sort keys of dtype {dt}")
+
+
+def _sortable_tensor(t: Any):
+    """The same for CUDA tensors (torch ops on the device)."""
+    import torch
+
+    if t.dtype in (torch.int32, torch.int64) or t.dtype in (getattr(torch, "uint32", None), getattr(torch, "uint64", None)):
+        return t, lambda k: k
+    if t.dtype in (torch.uint8, torch.bool):
+        return t.to(torch.int32), lambda k: k.to(t.dtype)
+    if t.dtype in (torch.int8, torch.int16):
+        return t.to(torch.int32), lambda k: k.to(t.dtype)
+    if t.dtype in (torch.float16, torch.bfloat16, torch.float32, torch.float64):
+        src = t if t.dtype in (torch.float32, torch.float64) else t.to(torch.float32)
+        st = torch.int64 if src.dtype == torch.float64 else torch.int32
+        low = torch.iinfo(st).max  # every bit but the sign
+        shift = 8 * src.element_size() - 1
+        # negative floats: flip all but the sign bit → the signed integer order
+        # is the float order; the map is its own inverse
+        keys = src.view(st) ^ ((src.view(st) >> shift) & low)
+
+        def back(k):
+            return (k ^ ((k >> shift) & low)).view(src.dtype).to(t.dtype)
+
+        return keys, back
+    raise TypeError(f"cannot sort keys of dtype {t.dtype}")
 
 
 def sample_sort_hybrid(
@@ -326,8 +376,9 @@ def sample_sort_hybrid(
     if fraction <= 0.0:
         # every bin on DeviceB: one GPU sort; a constant array is the
         # reference's lo == hi early return (work on DeviceA)
-        out = arr.clone() if dev else _gpu_keys(arr)
-        out, _, passes = sharding.run_sharded_sort(out)
+        keys, back = _sortable_tensor(arr) if dev else _sortable(arr)
+        out, _, passes = sharding.run_sharded_sort(keys.clone() if dev and keys is arr else keys)
+        out = back(out)
         if passes == 0:
             return out, float(n), 0.0
         return out, 0.0, float(n)
@@ -344,7 +395,8 @@ def sample_sort_hybrid(
 
     with ThreadPoolExecutor(max_workers=2) as pool:
         fa = pool.submit(np.sort, part_a, kind="quicksort")
-        fb = pool.submit(inherit_device(lambda: sharding.to_numpy(sharding.run_sharded_sort(_gpu_keys(part_b))[0])))
+        keys_b, back_b = _sortable(part_b)
+        fb = pool.submit(inherit_device(lambda: back_b(sharding.to_numpy(sharding.run_sharded_sort(keys_b)[0]))))
         sorted_a, sorted_b = fa.result(), fb.result()
     out = np.empty_like(host)
     pos = pa = pb = 0
@@ -632,6 +684,9 @@ def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out
     if is_device_array(pixels):
         import torch
 
+        # the host path's cast (np.ascontiguousarray(..., dtype=uint8)); the
+        # kernel reads raw contiguous uint8 rows
+        pixels = pixels.to(torch.uint8).contiguous()
         tdt = torch.float64 if code == 64 else torch.float32
         if out is None:
             out = torch.empty((row1 - row0, width), dtype=tdt, device=pixels.device)

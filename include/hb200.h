@@ -128,6 +128,17 @@ int hb_csr_validate(const void* row_ptr, int ptr_code, const void* col_idx, int 
                     int64_t rows, int64_t nnz, int64_t cols, uint32_t* flags_out, int flags,
                     void* stream);
 
+/* Device gen_csr (datasets.py:37-55), bit-identical to the reference:
+ * avg = max(1, round(density*cols)) (computed by the caller, Python's
+ * round), seed_counts/rows/vals = mix_seed(seed, 1/2/3) (rng.py:54-57).
+ * row_ptr (rows+1, ptr_code) is always written and *nnz_out returned; with
+ * col_idx == values == NULL nothing else happens (sizing call), otherwise
+ * col_idx/values (nnz_cap entries) receive the columns and values.  Rows of
+ * up to 1020 nonzeros; device pointers only.                                */
+int hb_gen_csr(int64_t rows, int64_t cols, int64_t avg, uint64_t seed_counts, uint64_t seed_rows,
+               uint64_t seed_vals, void* row_ptr, int ptr_code, void* col_idx, int col_code, double* values,
+               int64_t nnz_cap, int64_t* nnz_out, int flags, void* stream);
+
 /* ---------------------------------------------------------------- bilateral
  * Replaces bilateral_rows / BilateralApplyWorkload.run_part
  * (kernels_regular.py:461-511): output rows [row0, row1) of the clamp-to-edge

@@ -24,6 +24,9 @@
 // HB_SPMV_WARP: warp-per-row tree reduction (one FMA-free product per lane,
 // shuffle reduction): not bit-exact, within 1e-9 relative of the reference.
 #include <stdlib.h>
+
+#include <algorithm>
+#include <type_traits>
 #include <string.h>
 
 #include <thread>
@@ -895,6 +898,179 @@ extern "C" int hb_spmv_preprocess(const void* row_ptr, int ptr_code, const void*
   else if (c4) rc = q4 ? HB_PP(int64_t, int32_t, int32_t) : HB_PP(int64_t, int32_t, int64_t);
   else rc = q4 ? HB_PP(int64_t, int64_t, int32_t) : HB_PP(int64_t, int64_t, int64_t);
 #undef HB_PP
+  if (rc != HB_OK) return rc;
+  return finish(flags, s);
+}
+
+// ------------------------------------------------------------------ gen_csr
+// Device gen_csr (reference datasets.py:37-55), bit-identical:
+//   counts[r] = min(1 + draw_{r+1}(mix_seed(s,1)) % (2·avg-1), cols)
+//   row r's column draws come from one sequential stream SplitMix64(mix_seed(s,2)):
+//     its seed is draw (r + 1 + retries so far) of that stream, its 2k+8
+//     candidates are draws 1..2k+8 of that seed, % cols; the row keeps the
+//     k smallest distinct values (np.unique(...)[:k]); a row with fewer than
+//     k distinct candidates takes further stream draws (the retry loop), which
+//     shifts every later row's seed by one draw per retry;
+//   values = 2·uniform_floats(mix_seed(s,3), nnz) - 1.
+// Warp per row: candidates in shared memory, distinct ranks by counting
+// (O(m²) compares on broadcast reads — m ≤ 70 at the 1M config), first
+// occurrence owns the slot.  Rows needing a retry (vanishingly rare unless
+// cols is tiny) are found in one pass; the first one is replayed on the
+// host exactly like the reference and the pass resumes after it.
+namespace hb {
+namespace {
+
+constexpr int kGenWarps = 4;
+constexpr int kGenMaxM = 2048;  // 2k+8 candidates per row: k <= 1020
+
+__global__ void gen_counts_kernel(uint64_t seed, int64_t rows, uint64_t bound, int64_t cols,
+                                  uint32_t* __restrict__ counts) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = 1 + (int64_t)(splitmix64_at(seed, (uint64_t)r + 1) % bound);
+    counts[r] = (uint32_t)(c < cols ? c : cols);
+  }
+}
+
+template <typename P, typename C>
+__global__ void __launch_bounds__(kGenWarps * 32)
+    gen_csr_rows_kernel(const P* __restrict__ rp, int64_t r_begin, int64_t rows, uint64_t seed_rows, int64_t shift,
+                        uint64_t cols, C* __restrict__ col, unsigned long long* __restrict__ first_bad) {
+  __shared__ uint32_t cand[kGenWarps][kGenMaxM];
+  __shared__ uint8_t first[kGenWarps][kGenMaxM];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warps = (int64_t)gridDim.x * kGenWarps;
+  uint32_t* cv = cand[w];
+  uint8_t* fv = first[w];
+  for (int64_t r = r_begin + (int64_t)blockIdx.x * kGenWarps + w; r < rows; r += warps) {
+    const int64_t base = (int64_t)rp[r];
+    const int k = (int)((int64_t)rp[r + 1] - base);
+    const int m = 2 * k + 8;
+    const uint64_t s = splitmix64_at(seed_rows, (uint64_t)(r + 1 + shift));
+    for (int i = lane; i < m; i += 32) cv[i] = (uint32_t)(splitmix64_at(s, (uint64_t)i + 1) % cols);
+    __syncwarp();
+    int distinct = 0;
+    for (int i = lane; i < m; i += 32) {
+      const uint32_t v = cv[i];
+      bool f = true;
+      for (int j = 0; j < i; ++j) f &= cv[j] != v;
+      fv[i] = f;
+      distinct += f;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, o);
+    __syncwarp();
+    if (distinct < k) {
+      if (lane == 0) atomicMin(first_bad, (unsigned long long)r);
+    } else {
+      for (int i = lane; i < m; i += 32) {
+        if (!fv[i]) continue;
+        const uint32_t v = cv[i];
+        int rank = 0;
+        for (int j = 0; j < m; ++j) rank += (fv[j] && cv[j] < v);
+        if (rank < k) col[base + rank] = (C)v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void gen_values_kernel(uint64_t seed, int64_t n, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = (double)(splitmix64_at(seed, (uint64_t)i + 1) >> 11) * 0x1p-53;
+    out[i] = __dadd_rn(__dmul_rn(2.0, u), -1.0);
+  }
+}
+
+template <typename P, typename C>
+int gen_csr_impl(int64_t rows, int64_t cols, uint64_t bound, uint64_t seed_counts, uint64_t seed_rows,
+                 uint64_t seed_vals, P* rp, C* col, double* vals, int64_t nnz_cap, int64_t* nnz_out, cudaStream_t s) {
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  DevBuf counts, sums, bad;
+  HB_TRY(alloc(&counts, (size_t)rows * 4, s));
+  int64_t g = ceil_div(rows, 256);
+  if (g > (int64_t)di.sms * 16) g = (int64_t)di.sms * 16;
+  gen_counts_kernel<<<(int)g, 256, 0, s>>>(seed_counts, rows, bound, cols, counts.as<uint32_t>());
+  const int64_t nb = ceil_div(rows, kScanTile);
+  HB_TRY(alloc(&sums, (size_t)(nb + 1) * 8, s));
+  scan_tile_sums<<<(unsigned)nb, kScanT, 0, s>>>(counts.as<uint32_t>(), rows, sums.as<int64_t>());
+  scan_sums_serial<<<1, 1, 0, s>>>(sums.as<int64_t>(), nb);
+  scan_tile_apply<P><<<(unsigned)nb, kScanT, 0, s>>>(counts.as<uint32_t>(), rows, sums.as<int64_t>(), rp);
+  HB_TRY(check_launch());
+  int64_t nnz = 0;
+  HB_CUDA_TRY(cudaMemcpyAsync(&nnz, sums.as<int64_t>() + nb, 8, cudaMemcpyDeviceToHost, s));
+  HB_CUDA_TRY(cudaStreamSynchronize(s));
+  *nnz_out = nnz;
+  if (col == nullptr) return HB_OK;  // sizing call
+  HB_CHECK_ARG(nnz_cap >= nnz, "col/values hold %lld entries, need %lld", (long long)nnz_cap, (long long)nnz);
+  if (std::is_same<P, int32_t>::value) HB_CHECK_ARG(nnz < (1ll << 31), "nnz needs an int64 row_ptr");
+  // rows denser than the shared-memory candidate buffer are not supported
+  const uint64_t max_k = cols < (int64_t)bound + 1 ? (uint64_t)cols : bound;
+  HB_CHECK_ARG(2 * max_k + 8 <= (uint64_t)kGenMaxM, "rows of up to %d nonzeros are supported on the device",
+               (kGenMaxM - 8) / 2);
+  HB_TRY(alloc(&bad, 8, s));
+  int64_t gw = ceil_div(rows, kGenWarps);
+  if (gw > (int64_t)di.sms * 8) gw = (int64_t)di.sms * 8;
+  int64_t r_begin = 0, shift = 0;
+  while (r_begin < rows) {
+    const unsigned long long none = ~0ull;
+    HB_CUDA_TRY(cudaMemcpyAsync(bad.ptr, &none, 8, cudaMemcpyHostToDevice, s));
+    gen_csr_rows_kernel<P, C><<<(int)gw, kGenWarps * 32, 0, s>>>(rp, r_begin, rows, seed_rows, shift,
+                                                                  (uint64_t)cols, col, bad.as<unsigned long long>());
+    HB_TRY(check_launch());
+    unsigned long long first_bad = none;
+    HB_CUDA_TRY(cudaMemcpyAsync(&first_bad, bad.ptr, 8, cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (first_bad == none) break;
+    // replay row `r` exactly like the reference: union of the candidates of
+    // successive stream draws until k distinct values exist; keep the k smallest
+    const int64_t r = (int64_t)first_bad;
+    P ends[2];
+    HB_CUDA_TRY(cudaMemcpyAsync(ends, rp + r, 2 * sizeof(P), cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t k = (int64_t)ends[1] - (int64_t)ends[0];
+    std::vector<uint64_t> chosen;
+    int64_t draw = r + 1 + shift;
+    for (;;) {
+      const uint64_t sd = splitmix64_at(seed_rows, (uint64_t)draw);
+      for (int64_t i = 1; i <= 2 * k + 8; ++i) chosen.push_back(splitmix64_at(sd, (uint64_t)i) % (uint64_t)cols);
+      std::sort(chosen.begin(), chosen.end());
+      chosen.erase(std::unique(chosen.begin(), chosen.end()), chosen.end());
+      if ((int64_t)chosen.size() >= k) break;
+      ++draw;
+      ++shift;
+    }
+    std::vector<C> row((size_t)k);
+    for (int64_t i = 0; i < k; ++i) row[(size_t)i] = (C)chosen[(size_t)i];
+    HB_CUDA_TRY(cudaMemcpyAsync(col + (int64_t)ends[0], row.data(), (size_t)k * sizeof(C), cudaMemcpyHostToDevice, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    r_begin = r + 1;
+  }
+  int64_t gv = ceil_div(nnz, 256);
+  if (gv > (int64_t)di.sms * 16) gv = (int64_t)di.sms * 16;
+  if (nnz) gen_values_kernel<<<(int)gv, 256, 0, s>>>(seed_vals, nnz, vals);
+  return check_launch();
+}
+
+}  // namespace
+}  // namespace hb
+
+extern "C" int hb_gen_csr(int64_t rows, int64_t cols, int64_t avg, uint64_t seed_counts, uint64_t seed_rows,
+                          uint64_t seed_vals, void* row_ptr, int ptr_code, void* col_idx, int col_code,
+                          double* values, int64_t nnz_cap, int64_t* nnz_out, int flags, void* stream) {
+  using namespace hb;
+  HB_CHECK_ARG(rows >= 1 && rows < (1ll << 31) && cols >= 1 && cols <= (1ll << 31), "matrix shape out of range");
+  HB_CHECK_ARG(avg >= 1, "avg must be >= 1");
+  HB_CHECK_ARG(idx_size_ok(ptr_code) && idx_size_ok(col_code), "index arrays must be int32 or int64");
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_gen_csr writes device arrays");
+  HB_CHECK_ARG(row_ptr && nnz_out && (!col_idx == !values), "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t bound = (uint64_t)(2 * avg - 1 > 1 ? 2 * avg - 1 : 1);
+  int rc;
+#define HB_GC(P, C) gen_csr_impl<P, C>(rows, cols, bound, seed_counts, seed_rows, seed_vals, (P*)row_ptr, (C*)col_idx, values, nnz_cap, nnz_out, s)
+  if (ptr_code == HB_I32) rc = col_code == HB_I32 ? HB_GC(int32_t, int32_t) : HB_GC(int32_t, int64_t);
+  else rc = col_code == HB_I32 ? HB_GC(int64_t, int32_t) : HB_GC(int64_t, int64_t);
+#undef HB_GC
   if (rc != HB_OK) return rc;
   return finish(flags, s);
 }

@@ -229,6 +229,39 @@ def device_gen_list(n: int, seed: int, succ_dtype=np.int32):
     return succ, head
 
 
+def device_gen_csr(rows: int, cols: int, seed: int, density: float, index_dtype=np.int32):
+    """gen_csr in HBM (hb_gen_csr), bit-identical to the reference
+    (datasets.py:37-55) and to `csr_arrays`: a device CsrMatrix with int32
+    (default) or int64 row_ptr / col_idx and float64 values."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .gpu import current_stream_handle, vp
+    from .kernels_irregular import CsrMatrix
+
+    avg = max(1, round(density * cols))
+    seeds = [mix_seed(seed, salt) & MASK64 for salt in (1, 2, 3)]
+    tdt = torch.int32 if np.dtype(index_dtype) == np.int32 else torch.int64
+    code = _lib.DTYPE_CODES["i4" if tdt == torch.int32 else "i8"]
+    rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+    nnz = ctypes.c_int64(0)
+    st = current_stream_handle(rp)
+    _lib.call("hb_gen_csr", rows, cols, avg, *seeds, vp(rp.data_ptr()), _lib.DTYPE_CODES["i8"], None, code, None, 0,
+              ctypes.byref(nnz), _lib.HB_DEVICE_PTRS, st)
+    nnz = nnz.value
+    ptr_t = tdt if nnz < 2**31 else torch.int64
+    rp = torch.empty(rows + 1, dtype=ptr_t, device="cuda")
+    col = torch.empty(nnz, dtype=tdt, device="cuda")
+    val = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    out = ctypes.c_int64(0)
+    _lib.call("hb_gen_csr", rows, cols, avg, *seeds, vp(rp.data_ptr()),
+              _lib.DTYPE_CODES["i4" if ptr_t == torch.int32 else "i8"], vp(col.data_ptr()), code, vp(val.data_ptr()),
+              nnz, ctypes.byref(out), _lib.HB_DEVICE_PTRS, st)
+    return CsrMatrix(rows, cols, rp, col, val)
+
+
 def device_gen_sort_data(n: int, seed: int, k0: int = 0):
     """gen_sort_data in HBM: uint32 keys (draw >> 32) of draws k0+1..k0+n,
     as an int32 tensor holding the same bits."""

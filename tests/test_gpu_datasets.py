@@ -46,3 +46,26 @@ def test_worker_threads_inherit_the_callers_device():
     t.join()
     torch.cuda.set_device(0)
     assert seen == [last]
+
+
+@pytest.mark.parametrize("rows,cols,seed,density", [
+    (100_000, 100_000, 42, 1.6e-4),   # ~16 nnz/row, like the 1M config
+    (20_000, 1_000_000, 7, 1.6e-5),
+    (5_000, 50, 3, 0.2),              # dense-ish rows (up to 19 of 50 columns)
+    (3_000, 10, 5, 0.5),              # 10 columns: rows that need the retry loop
+    (1, 1, 9, 1.0),
+])
+def test_device_gen_csr_matches_reference_generator(rows, cols, seed, density):
+    """hb_gen_csr == csr_arrays (itself pinned to the reference's gen_csr by
+    the golden fixtures), including rows that take extra stream draws."""
+    ptr, col, val = d.csr_arrays(rows, cols, seed, density)
+    for idx in (np.int32, np.int64):
+        m = d.device_gen_csr(rows, cols, seed, density, idx)
+        assert np.array_equal(m.row_ptr.cpu().numpy().astype(np.int64), ptr)
+        assert np.array_equal(m.col_idx.cpu().numpy().astype(np.int64), col)
+        assert np.array_equal(m.values.cpu().numpy().view(np.uint64), val.view(np.uint64))
+
+
+def test_device_gen_csr_at_config_size():
+    m = d.device_gen_csr(1_000_000, 1_000_000, 42, 1.6e-5)
+    assert m.nnz == 15_989_277  # the reference's nnz at the SpMV config (SURVEY §8a)

@@ -291,7 +291,7 @@ def _all_workloads(rank, world):
         # measured calibration agrees across ranks (same fraction everywhere)
         sh = calibrate_measured(kr.HistogramWorkload(data, 256), p, max_refinements=2, repeats=1)
         fr = sharding.all_gather_small(torch.tensor([sh.fraction_a], dtype=torch.float64, device="cuda"), g)
-        res["calibrate_agrees"] = len(set(fr.cpu().tolist())) == 1
+        res["calibrate_agrees"] = len(set(fr.reshape(-1).cpu().tolist())) == 1
     bad = sorted(k for k, v in res.items() if not v)
     return True if not bad else f"failed: {bad}"
 

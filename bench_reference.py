@@ -1,14 +1,16 @@
-"""The reference arm of bench.py: the UNMODIFIED reference package
+"""The reference side of bench.py: the UNMODIFIED reference package
 (`hybridbench`, installed under baseline/_ref with
 `pip install --no-index --no-deps --target baseline/_ref <copy of /root/reference/pkg>`)
 timed through its own public entry points on the host cores.
 
-Nothing here imports torch, libhb200 or the product package: inputs are made
-by the threaded numpy splitmix64 below (the reference's own generators for
-the irregular workloads), so the reference arm loads no native code of this
-repository.  When baseline/_ref is absent (e.g. a fresh checkout), the
-numpy restatement under oracle/ is timed instead and the line says
-`kind: "port"`.
+Used twice: `bench.py --impl reference` (the reference arm: inputs made
+here with the threaded numpy splitmix64 below or the reference's own
+generators — nothing imports torch, libhb200 or the product package, so
+that arm loads no native code of this repository), and bench.py's
+`cpu_baseline` legs (the same reference calls on host copies of the very
+inputs the GPU arm ran on).  When baseline/_ref is absent (a fresh
+checkout) the numpy restatement under oracle/ is timed instead and the
+line says `kind: "port"`.
 
 Each leg returns (fn, units, sample, cores, kind, same_config): `fn()` runs
 one step of the reference on its input; `units / t` is the metric.
@@ -70,22 +72,23 @@ def splitmix_low8(seed: int, n: int, k0: int = 0, threads: int | None = None) ->
     return out
 
 
-def _platform(ref):
+def _platform():
     from hybridbench.platform import Accounting, Platform
 
     return Platform.build(1.0, 3.0, accounting=Accounting.MEASURED)
 
 
 # ------------------------------------------------------------------ legs
+# `x`, `keys`, ... : host inputs to reuse (cpu_baseline legs); None → made here
 
 
-def hist_leg(n: int, seed: int = 42, bins: int = 256):
-    x = splitmix_low8(seed, n)
+def hist_leg(n: int, x: np.ndarray | None = None, seed: int = 42, bins: int = 256):
+    x = splitmix_low8(seed, n) if x is None else x
     if reference_available():
-        ref = import_reference()
+        import_reference()
         from hybridbench.kernels_regular import hybrid_histogram
 
-        p = _platform(ref)
+        p = _platform()
         fn = lambda: hybrid_histogram(x, bins, p)  # noqa: E731
         kind = "reference"
     else:
@@ -93,66 +96,73 @@ def hist_leg(n: int, seed: int = 42, bins: int = 256):
 
         fn = lambda: ohist.hybrid(x, bins, 0.25)  # noqa: E731
         kind = "port"
-    sample = f"full config: 2^{n.bit_length() - 1} uint8, hybrid_histogram, formula share 0.25 (2 side threads)"
-    return fn, n, sample, 2, kind, True
+    m = x.size
+    sample = f"2^{m.bit_length() - 1} uint8 through hybrid_histogram, formula share 0.25 (2 side threads)"
+    return fn, m, sample, 2, kind, m == n
 
 
-def sort_leg(n: int, seed: int = 42, sample_n: int = 1 << 20):
+def sort_leg(n: int, keys: np.ndarray | None = None, seed: int = 42, sample_n: int = 1 << 20):
     m = min(n, sample_n)
-    ref = import_reference() if reference_available() else None
-    if ref is not None:
+    if reference_available():
+        import_reference()
         from hybridbench.datasets import gen_sort_data
         from hybridbench.kernels_regular import sample_sort_hybrid
 
-        keys = gen_sort_data(m, seed).astype(np.uint32)
-        p = _platform(ref)
-        fn = lambda: sample_sort_hybrid(keys, p)  # noqa: E731
+        k = gen_sort_data(m, seed).astype(np.uint32) if keys is None else keys[:m]
+        p = _platform()
+        fn = lambda: sample_sort_hybrid(k, p)  # noqa: E731
         kind = "reference"
     else:
         from oracle import datasets as ods
         from oracle import sort as osort
 
-        keys = ods.sort_keys(m, seed).astype(np.int64)
-        fn = lambda: osort.sample_sort_hybrid(keys, 0.25)  # noqa: E731
+        k = (ods.sort_keys(m, seed) if keys is None else keys[:m]).astype(np.int64)
+        fn = lambda: osort.sample_sort_hybrid(k, 0.25)  # noqa: E731
         kind = "port"
-    return fn, m, f"2^{m.bit_length() - 1} uint32 keys of gen_sort_data(n, 42), sample_sort_hybrid (keys only), formula share 0.25", 2, kind, m == n
+    return (fn, m, f"2^{m.bit_length() - 1} uint32 keys of gen_sort_data(n, 42), sample_sort_hybrid (keys only)", 2,
+            kind, m == n)
 
 
-def spmv_leg(rows: int, density: float, seed: int = 42):
-    ref = import_reference() if reference_available() else None
-    if ref is not None:
+def spmv_leg(rows: int, density: float, arrays=None, x: np.ndarray | None = None, seed: int = 42):
+    """arrays = (row_ptr, col_idx, values) int64/int64/f64 of gen_csr(rows,
+    rows, seed, density) when the caller has them (bit-identical)."""
+    if reference_available():
+        import_reference()
         from hybridbench.datasets import gen_csr
-        from hybridbench.kernels_irregular import spmv_hybrid, spmv_preprocess
+        from hybridbench.kernels_irregular import CsrMatrix, spmv_hybrid, spmv_preprocess
         from hybridbench.rng import mix_seed, uniform_floats
 
-        m = gen_csr(rows, rows, seed, density)
-        x = 2.0 * uniform_floats(mix_seed(seed, 0xDEC0), rows) - 1.0
-        prep = spmv_preprocess(m, _platform(ref))
+        m = gen_csr(rows, rows, seed, density) if arrays is None else CsrMatrix(rows, rows, *arrays)
+        xx = 2.0 * uniform_floats(mix_seed(seed, 0xDEC0), rows) - 1.0 if x is None else x
+        prep = spmv_preprocess(m, _platform())
         nnz = m.nnz
-        fn = lambda: spmv_hybrid(prep, x)  # noqa: E731
+        fn = lambda: spmv_hybrid(prep, xx)  # noqa: E731
         kind = "reference"
     else:
         from oracle import datasets as ods
         from oracle import rng as orng
         from oracle import spmv as ospmv
 
-        ptr, col, val = ods.csr(rows, rows, seed, density)
-        x = 2.0 * orng.uniform_floats(orng.mix_seed(seed, 0xDEC0), rows) - 1.0
+        ptr, col, val = ods.csr(rows, rows, seed, density) if arrays is None else arrays
+        xx = 2.0 * orng.uniform_floats(orng.mix_seed(seed, 0xDEC0), rows) - 1.0 if x is None else x
         perm, permuted, split = ospmv.preprocess(ptr, col, val, 1.0, 3.0, None)
         nnz = int(ptr[-1])
-        fn = lambda: ospmv.hybrid(perm, permuted, split, x)  # noqa: E731
+        fn = lambda: ospmv.hybrid(perm, permuted, split, xx)  # noqa: E731
         kind = "port"
-    return fn, 2 * nnz, f"full config: gen_csr({rows}, {rows}, 42, {density}), spmv_hybrid (prep untimed), modeled split", 2, kind, True
+    return (fn, 2 * nnz, f"gen_csr({rows}, {rows}, 42, {density}), spmv_hybrid (prep untimed), modeled split", 2,
+            kind, True)
 
 
-def filter_leg(kind_name: str, side: int, radius: int, rows: int = 64, seed: int = 42):
-    img = splitmix_low8(seed, (rows + radius) * side).reshape(rows + radius, side)[:rows]
-    img = np.ascontiguousarray(img)
-    ref = import_reference() if reference_available() else None
-    if ref is not None:
+def filter_leg(kind_name: str, side: int, radius: int, img: np.ndarray | None = None, rows: int = 64,
+               seed: int = 42):
+    if img is None:
+        img = splitmix_low8(seed, (rows + radius) * side).reshape(rows + radius, side)
+    img = np.ascontiguousarray(img[:rows])
+    if reference_available():
+        import_reference()
         from hybridbench.kernels_regular import FilterKernel, Image, build_bilateral_lut, hybrid_bilateral, hybrid_convolve
 
-        p = _platform(ref)
+        p = _platform()
         if kind_name == "bilat":
             lut = build_bilateral_lut(radius, max(radius / 2.0, 0.5), 40.0)
             fn = lambda: hybrid_bilateral(Image(img), lut, p)  # noqa: E731
@@ -175,18 +185,18 @@ def filter_leg(kind_name: str, side: int, radius: int, rows: int = 64, seed: int
             fn = lambda: oconv.hybrid(img, w, 0.25)  # noqa: E731
         kind = "port"
     what = "hybrid_bilateral" if kind_name == "bilat" else "hybrid_convolve"
-    return fn, rows * side, f"{rows} x {side} strip of gen_image({side}, 42), {what}, formula share 0.25", 2, kind, False
+    return fn, rows * side, f"{rows} x {side} strip of gen_image({side}, 42), {what}", 2, kind, False
 
 
 def lr_leg(n: int, seed: int = 42, sample_n: int = 1 << 20):
     m = min(n, sample_n)
-    ref = import_reference() if reference_available() else None
-    if ref is not None:
+    if reference_available():
+        import_reference()
         from hybridbench.datasets import gen_list
         from hybridbench.kernels_irregular import list_rank_with_stats
 
         lst = gen_list(m, seed)
-        p = _platform(ref)
+        p = _platform()
         fn = lambda: list_rank_with_stats(lst, p, seed)  # noqa: E731
         kind = "reference"
     else:
@@ -196,4 +206,4 @@ def lr_leg(n: int, seed: int = 42, sample_n: int = 1 << 20):
         succ, head = ods.linked_list(m, seed)
         fn = lambda: olr.list_rank_with_stats(succ, head, seed)  # noqa: E731
         kind = "port"
-    return fn, m, f"gen_list(2^{m.bit_length() - 1}, 42), list_rank_with_stats (validate + FIS + sublists)", 1, kind, m == n
+    return fn, m, f"gen_list(2^{m.bit_length() - 1}, 42), list_rank_with_stats", 1, kind, m == n

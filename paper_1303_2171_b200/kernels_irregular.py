@@ -419,8 +419,9 @@ def _spmv_device(prep: SpmvPrep, x: Any) -> Any:
     split = prep.split_row
     y = torch.empty(m.rows, dtype=torch.float64, device=xd.device)
     g = sharding.active_group()
-    with ThreadPoolExecutor(max_workers=1) as pool:
-        fa = pool.submit(_host_range_matvec, m.to_host(), np.asarray(to_host(xd)), 0, split, prep.workers_a) if split else None
+    pool = ThreadPoolExecutor(max_workers=1) if split else None  # the host share runs beside the GPU rows
+    try:
+        fa = pool.submit(_host_range_matvec, m.to_host(), np.asarray(to_host(xd)), 0, split, prep.workers_a) if pool else None
         if split < m.rows:
             if sharding.multi(g):
                 scatter_perm(_gpu_rows(m, xd, split, m.rows), perm[split:], y)
@@ -428,6 +429,9 @@ def _spmv_device(prep: SpmvPrep, x: Any) -> Any:
                 gpu_spmv(m, xd, split, m.rows, y=y, perm=perm)
         if fa is not None:
             scatter_perm(torch.from_numpy(fa.result()).to(y.device), perm[:split], y)
+    finally:
+        if pool is not None:
+            pool.shutdown()
     return y if is_device_array(x) else y.cpu().numpy()
 
 

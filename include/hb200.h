@@ -171,7 +171,16 @@ int hb_convolve(const void* img, int in_code, int32_t height, int32_t width, int
  * HB_U32/HB_I32/HB_U64/HB_I64).  When vals_in/vals_out are non-NULL the
  * uint32 payload is permuted alongside — stably, so a payload of 0..n-1
  * becomes the stable argsort.  *passes_done (optional) receives the number
- * of digit passes executed (0 ⇔ all keys equal).  n < 2^30 per call.      */
+ * of digit passes executed (0 ⇔ all keys equal).  n < 2^30 per call.
+ * Ranking: one shared atomic per key, relying on lane-ordered old values
+ * (verified on each device before first use; the ballot multi-split runs
+ * when the check fails).  flags & HB_SORT_BALLOT (or HB_SORT_RANK=ballot in
+ * the environment) selects the ballot multi-split, whose stability does not
+ * depend on that behaviour — the library's own stable-argsort users
+ * (device gen_list, spmv_preprocess) use it.  With HB_ASYNC and
+ * passes_done == NULL (32-bit keys) the call never waits on the host: all
+ * four digit positions are sorted.                                         */
+#define HB_SORT_BALLOT 8  /* rank with the ballot multi-split instead of lane-ordered shared atomics */
 int hb_sort(const void* keys_in, void* keys_out, int key_code, const uint32_t* vals_in,
             uint32_t* vals_out, int64_t n, int32_t* passes_done, int flags, void* stream);
 

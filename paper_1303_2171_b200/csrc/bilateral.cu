@@ -102,104 +102,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
 }
 
-// Persistent variant (HB_BILAT_CFG=3; measured no faster than one CTA per
-// tile, kept for the record): grid = 2 CTAs per SM, each CTA walks
-// tiles round-robin.  The lane-striped range table is built once per CTA
-// (not once per tile), and the halo of the NEXT tile is loaded into
-// registers before the current tile is filtered and written to the other
-// shared-memory buffer afterwards, so the global-load latency of the halo
-// is hidden behind the fp64 work instead of stalling every tile.
-template <int R, typename OUT>
-__global__ void __launch_bounds__(kThreads, 2)
-    bilateral_persist_kernel(const uint8_t* __restrict__ img, int H, int W, int row0, int row1,
-                             const double* __restrict__ spatial, const double* __restrict__ range,
-                             OUT* __restrict__ out, int tiles_x, int ntiles) {
-  constexpr int S = 2 * R + 1;
-  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
-  constexpr int HALO = TH * TW;
-  constexpr int PER = (HALO + kThreads - 1) / kThreads;  // halo pixels per thread
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* rng = reinterpret_cast<double*>(smem);  // [256][32] lane-striped
-  double* sp = rng + 256 * 32;                    // [S*S]
-  int* tiles = reinterpret_cast<int*>(sp + S * S);  // [2][TH][TW]
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  for (int i = tid; i < 256 * 32; i += kThreads) rng[i] = range[i >> 5];
-  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
-
-  int pre[PER];
-  auto fetch = [&](int t) {  // halo of tile t into registers (clamped)
-    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + u * kThreads;
-      if (i < HALO) {
-        const int ty = i / TW, tx = i - ty * TW;
-        const int gy = min(max(y0 - R + ty, 0), H - 1);
-        const int gx = min(max(x0 - R + tx, 0), W - 1);
-        pre[u] = img[(int64_t)gy * W + gx];
-      }
-    }
-  };
-  auto stash = [&](int* buf) {
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + u * kThreads;
-      if (i < HALO) buf[i] = pre[u];
-    }
-  };
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
-  fetch(t);
-  stash(tiles);
-  __syncthreads();
-  const int py = tid / (kTileW / kPx);
-  const int px = (tid % (kTileW / kPx)) * kPx;
-  const double* lane_rng = rng + lane;
-  for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) fetch(tn);  // in flight while this tile is filtered
-    const int* tile = tiles + b * HALO;
-    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
-    const int gy = y0 + py;
-    if (gy < row1) {
-      int c[kPx];
-#pragma unroll
-      for (int j = 0; j < kPx; ++j) c[j] = tile[(py + R) * TW + px + j + R];
-      double num[kPx], den[kPx];
-#pragma unroll
-      for (int j = 0; j < kPx; ++j) num[j] = den[j] = 0.0;
-#pragma unroll 1
-      for (int dy = 0; dy < S; ++dy) {
-        int nb[kPx + 2 * R];
-        double nbd[kPx + 2 * R];
-        const int* trow = tile + (py + dy) * TW + px;
-#pragma unroll
-        for (int k = 0; k < kPx + 2 * R; ++k) {
-          nb[k] = trow[k];
-          nbd[k] = (double)nb[k];
-        }
-#pragma unroll
-        for (int dx = 0; dx < S; ++dx) {
-          const double s = sp[dy * S + dx];
-#pragma unroll
-          for (int j = 0; j < kPx; ++j) {
-            const int d = abs(nb[j + dx] - c[j]);
-            const double w = __dmul_rn(s, lane_rng[d << 5]);
-            num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
-            den[j] = __dadd_rn(den[j], w);
-          }
-        }
-      }
-      OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
-#pragma unroll
-      for (int j = 0; j < kPx; ++j)
-        if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
-    }
-    if (tn < ntiles) stash(tiles + (b ^ 1) * HALO);
-    __syncthreads();
-  }
-}
 
 // TMA-staged variant (the default when the image allows a tensor map: row
 // pitch a multiple of 16 bytes, 16-byte aligned base): the halo tile of an
@@ -223,13 +125,8 @@ struct TmaTile {
 // NR output rows per thread (tile 32·NR x 64): a loaded tap row segment (and
 // its fp64 conversion) serves all NR rows; per pixel the taps stay in
 // row-major order, so the result is bit-identical.
-//
-// VEC (HB_BILAT_CFG=8): a thread's row segment (kPx + 2R bytes at an
-// unaligned offset) comes in as a few aligned 8-byte shared loads unpacked
-// with shifts instead of one byte load per neighbour — fewer shared-memory
-// wavefronts, but measured 2 % slower (26.5 vs 27.0 Gpix/s): the unpacking
-// costs more issue slots than the byte loads cost wavefronts.
-template <int R, typename OUT, int NR, int MINB, bool SYM = false, bool VEC = false>
+
+template <int R, typename OUT, int NR, int MINB, bool SYM = false>
 __global__ void __launch_bounds__(kThreads, MINB)
     bilateral_tma_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ img, int H, int W,
                          int row0, int row1, const double* __restrict__ spatial, const double* __restrict__ range,
@@ -304,19 +201,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     int nb[kPx + 2 * R];
     double nbd[kPx + 2 * R];
     const uint8_t* trow = tile + (py + iy) * TWB + px + OFF;
-    if (VEC) {
-      constexpr int LO = OFF & ~7, SH = OFF - LO, NW = (SH + kPx + 2 * R + 7) / 8;
-      static_assert((kTileW - kPx) + LO + 8 * NW <= TWB && TWB % 8 == 0 && kPx % 8 == 0, "aligned segment window");
-      const uint64_t* wrow = reinterpret_cast<const uint64_t*>(tile + (py + iy) * TWB + px + LO);
-      uint64_t wv[NW];
 #pragma unroll
-      for (int i = 0; i < NW; ++i) wv[i] = wrow[i];
-#pragma unroll
-      for (int q = 0; q < kPx + 2 * R; ++q) nb[q] = (int)((wv[(SH + q) >> 3] >> (((SH + q) & 7) * 8)) & 255u);
-    } else {
-#pragma unroll
-      for (int q = 0; q < kPx + 2 * R; ++q) nb[q] = trow[q];
-    }
+    for (int q = 0; q < kPx + 2 * R; ++q) nb[q] = trow[q];
 #pragma unroll
     for (int q = 0; q < kPx + 2 * R; ++q) {
       nbd[q] = (double)nb[q];
@@ -354,122 +240,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
-// Persistent variant (HB_BILAT_CFG=9): grid = SMs x MINB CTAs loop over the
-// tiles, so the 64 KB signed range table and the spatial weights are built
-// once per CTA instead of once per tile, and the halo tile of the NEXT tile
-// is requested by TMA (second 4 KB buffer, own mbarrier) before the current
-// one is filtered.  Same per-pixel arithmetic as bilateral_tma_kernel<SYM>.
-template <int R, typename OUT, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-    bilateral_tmap_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ img, int H, int W,
-                          int row0, int row1, const double* __restrict__ spatial,
-                          const double* __restrict__ range, OUT* __restrict__ out, int tiles_x, int ntiles) {
-  using T = TmaTile<R, 1>;
-  constexpr int S = 2 * R + 1;
-  constexpr int TH = T::TH, TW = T::TW, TWB = T::TWB, OFF = T::OFF;
-  constexpr int TBYTES = ((TH * TWB + 127) / 128) * 128;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
-  uint8_t* tiles = smem;                                             // [2][TBYTES]
-  double* rng = reinterpret_cast<double*>(smem + 2 * TBYTES);        // [511][16]
-  double* sp = rng + 511 * 16;                                       // [S*S]
-  const int tid = threadIdx.x;
-  const int lane = tid & 15;
-  auto origin = [&](int t, int& y0, int& x0) {
-    y0 = row0 + (t / tiles_x) * kTileH;
-    x0 = (t % tiles_x) * kTileW;
-  };
-  auto interior = [&](int y0, int x0) {
-    return x0 - T::PADX >= 0 && x0 - T::PADX + TWB <= W && y0 - R >= 0 && y0 - R + TH <= H;
-  };
-  auto request = [&](int t, int b) {  // thread 0: TMA the halo of tile t into buffer b when interior
-    int y0, x0;
-    origin(t, y0, x0);
-    if (!interior(y0, x0)) return;
-    fence_proxy_async_smem();
-    mbar_expect_tx(&bar[b], TH * TWB);
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(tiles + b * TBYTES);
-    const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&bar[b]);
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(d), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0 - T::PADX), "r"(y0 - R), "r"(bb) : "memory");
-  };
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if ((int)blockIdx.x < ntiles) request(blockIdx.x, 0);
-  }
-  for (int i = tid; i < 511 * 16; i += kThreads) rng[i] = range[abs((i >> 4) - 255)];
-  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
-  __syncthreads();
-  const double* lane_rng = rng + lane + 255 * 16;
-  const uint32_t lr = (uint32_t)__cvta_generic_to_shared(lane_rng);
-  const int py = tid / (kTileW / kPx);
-  const int px = (tid % (kTileW / kPx)) * kPx;
-  uint32_t ph[2] = {0u, 0u};
-  int b = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, b ^= 1) {
-    int y0, x0;
-    origin(t, y0, x0);
-    uint8_t* tile = tiles + b * TBYTES;
-    const bool in = interior(y0, x0);
-    if (tid == 0 && t + (int)gridDim.x < ntiles) request(t + gridDim.x, b ^ 1);  // next tile's halo
-    if (!in) {
-      for (int i = tid; i < TH * TW; i += kThreads) {
-        const int ty = i / TW, tx = i - ty * TW;
-        const int gy = min(max(y0 - R + ty, 0), H - 1);
-        const int gx = min(max(x0 - R + tx, 0), W - 1);
-        tile[ty * TWB + tx + OFF] = img[(int64_t)gy * W + gx];
-      }
-      __syncthreads();
-    } else {
-      mbar_wait(&bar[b], ph[b]);
-      ph[b] ^= 1u;
-    }
-    const int gy = y0 + py;
-    if (gy < row1) {
-      int c[kPx];
-      double num[kPx], den[kPx];
-      uint32_t cbase[kPx];
-#pragma unroll
-      for (int j = 0; j < kPx; ++j) {
-        c[j] = tile[(py + R) * TWB + px + j + R + OFF];
-        num[j] = den[j] = 0.0;
-        cbase[j] = lr - (uint32_t)c[j] * 128u;
-      }
-#pragma unroll 1
-      for (int dy = 0; dy < S; ++dy) {
-        int nb[kPx + 2 * R];
-        double nbd[kPx + 2 * R];
-        const uint8_t* trow = tile + (py + dy) * TWB + px + OFF;
-#pragma unroll
-        for (int q = 0; q < kPx + 2 * R; ++q) {
-          nb[q] = trow[q];
-          nbd[q] = (double)nb[q];
-          nb[q] *= 128;
-        }
-#pragma unroll
-        for (int dx = 0; dx < S; ++dx) {
-          const double sw = sp[dy * S + dx];
-#pragma unroll
-          for (int j = 0; j < kPx; ++j) {
-            double r;
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(cbase[j] + (uint32_t)nb[j + dx]));
-            const double w = __dmul_rn(sw, r);
-            num[j] = __dadd_rn(num[j], __dmul_rn(w, nbd[j + dx]));
-            den[j] = __dadd_rn(den[j], w);
-          }
-        }
-      }
-      OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
-#pragma unroll
-      for (int j = 0; j < kPx; ++j)
-        if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[j], den[j]);
-    }
-    __syncthreads();  // buffer b is free for the tile after next
-  }
-}
 
 // host: a 2-D uint8 tensor map over the image (driver entry point through
 // the runtime, no libcuda link); false when the layout does not allow one
@@ -522,83 +292,27 @@ template <int R, typename OUT>
 int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const double* sp,
                 const double* rg, OUT* out, cudaStream_t s) {
   constexpr int S = 2 * R + 1;
-  static const int variant = [] {
-    const char* e = getenv("HB_BILAT_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  if (variant == 0 || (variant >= 4 && variant <= 9)) {
-    // TMA-staged tiles.  default: one row per thread, symmetric 511-entry
-    // range table, 3 CTAs/SM; HB_BILAT_CFG 4: |d| table, 5: 2 rows, 6: 3 rows,
-    // 7: 2 rows with the symmetric table
-    auto launch_tma = [&](auto kern, auto tag, bool sym) -> int {
-      using T = decltype(tag);
-      CUtensorMap map;
-      if (!make_image_tmap(&map, img, H, W, T::TWB, T::TH)) return -1;
-      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + (sym ? 511 : 256) * 16 * 8 + S * S * 8;
+  // TMA-staged halo tiles, one row per thread, signed 511-entry range table
+  // striped over 16 lanes, 3 CTAs/SM (measured best)
+  {
+    using T = TmaTile<R, 1>;
+    auto kern = bilateral_tma_kernel<R, OUT, 1, 3, true>;
+    CUtensorMap map;
+    if (make_image_tmap(&map, img, H, W, T::TWB, T::TH)) {
+      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + 511 * 16 * 8 + S * S * 8;
       HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, T::TILE_H));
       kern<<<grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out);
       return check_launch();
-    };
-    int rc;
-    if (variant == 4) rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3>, TmaTile<R, 1>{}, false);
-    else if (variant == 5) rc = launch_tma(bilateral_tma_kernel<R, OUT, 2, 2>, TmaTile<R, 2>{}, false);
-    else if (variant == 6) rc = launch_tma(bilateral_tma_kernel<R, OUT, 3, 2>, TmaTile<R, 3>{}, false);
-    else if (variant == 7) rc = launch_tma(bilateral_tma_kernel<R, OUT, 2, 2, true>, TmaTile<R, 2>{}, true);
-    else if (variant == 8) rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3, true, true>, TmaTile<R, 1>{}, true);
-    else if (variant == 9) {
-      using TT = TmaTile<R, 1>;
-      CUtensorMap map;
-      if (!make_image_tmap(&map, img, H, W, TT::TWB, TT::TH)) {
-        rc = -1;
-      } else {
-        const size_t tb = (size_t)(TT::TH * TT::TWB + 127) / 128 * 128;
-        const size_t smem = 2 * tb + 511 * 16 * 8 + S * S * 8;
-        auto kern = bilateral_tmap_kernel<R, OUT, 3>;
-        HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        DeviceInfo di;
-        HB_TRY(device_info(&di));
-        const int tiles_x = (int)ceil_div(W, kTileW);
-        const int64_t ntiles = (int64_t)tiles_x * ceil_div(row1 - row0, kTileH);
-        HB_CHECK_ARG(ntiles < INT32_MAX, "image too large");
-        int64_t grid = (int64_t)di.sms * 3;
-        if (grid > ntiles) grid = ntiles;
-        kern<<<(unsigned)grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out, tiles_x, (int)ntiles);
-        rc = check_launch();
-      }
     }
-    else rc = launch_tma(bilateral_tma_kernel<R, OUT, 1, 3, true>, TmaTile<R, 1>{}, true);
-    if (rc != -1) return rc;  // -1: no tensor map for this layout, plain tiles below
   }
-  if (variant == 0 || variant == 2) {
-    // one CTA per tile, 16-lane striped table (46 KB smem), 3 CTAs per SM
-    const size_t smem = 256 * 16 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
-    auto k = variant == 0 ? bilateral_tile_kernel<R, OUT, 16, 3> : bilateral_tile_kernel<R, OUT, 16, 2>;
-    HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
-    k<<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out);
-    return check_launch();
-  }
-  if (variant == 3) {
-    const size_t smem = 256 * 32 * 8 + S * S * 8 + 2 * (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
-    HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_persist_kernel<R, OUT>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DeviceInfo di;
-    HB_TRY(device_info(&di));
-    const int tiles_x = (int)ceil_div(W, kTileW);
-    const int64_t ntiles = (int64_t)tiles_x * ceil_div(row1 - row0, kTileH);
-    HB_CHECK_ARG(ntiles < INT32_MAX, "image too large");
-    int64_t grid = (int64_t)di.sms * 2;
-    if (grid > ntiles) grid = ntiles;
-    bilateral_persist_kernel<R, OUT><<<(unsigned)grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out,
-                                                                            tiles_x, (int)ntiles);
-    return check_launch();
-  }
-  const size_t smem = 256 * 32 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
-  HB_CUDA_TRY(cudaFuncSetAttribute(bilateral_tile_kernel<R, OUT>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // no tensor map for this layout (row pitch not a multiple of 16 bytes):
+  // plain halo tiles loaded by the CTA, same arithmetic
+  const size_t smem = 256 * 16 * 8 + S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 4;
+  auto k = bilateral_tile_kernel<R, OUT, 16, 3>;
+  HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
-  bilateral_tile_kernel<R, OUT><<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out);
+  k<<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, sp, rg, out);
   return check_launch();
 }
 

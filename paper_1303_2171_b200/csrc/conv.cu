@@ -35,54 +35,6 @@ constexpr int kMaxR = 8;
 template <typename IN>
 __device__ __forceinline__ double to_f64(IN v) { return (double)v; }
 
-template <int R, typename IN, typename OUT, bool DENSE = false, int MINB = 2>
-__global__ void __launch_bounds__(kThreads, MINB)
-    conv_tile_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
-                     const double* __restrict__ weights, OUT* __restrict__ out) {
-  constexpr int S = 2 * R + 1;
-  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* sw = reinterpret_cast<double*>(smem);  // [S*S]
-  double* tile = sw + S * S;                     // [TH][TW]
-  const int tid = threadIdx.x;
-  const int y0 = row0 + blockIdx.y * kTileH;
-  const int x0 = blockIdx.x * kTileW;
-  for (int i = tid; i < S * S; i += kThreads) sw[i] = weights[i];
-  for (int i = tid; i < TH * TW; i += kThreads) {
-    const int ty = i / TW, tx = i - ty * TW;
-    const int gy = min(max(y0 - R + ty, 0), H - 1);
-    const int gx = min(max(x0 - R + tx, 0), W - 1);
-    tile[i] = to_f64(img[(int64_t)gy * W + gx]);
-  }
-  __syncthreads();
-  const int py = tid / (kTileW / kPx);
-  const int px = (tid % (kTileW / kPx)) * kPx;
-  const int gy = y0 + py;
-  if (gy >= row1) return;
-  double acc[kPx];
-#pragma unroll
-  for (int j = 0; j < kPx; ++j) acc[j] = 0.0;
-#pragma unroll 1
-  for (int dy = 0; dy < S; ++dy) {
-    double seg[kPx + 2 * R];
-    const double* trow = tile + (py + dy) * TW + px;
-#pragma unroll
-    for (int k = 0; k < kPx + 2 * R; ++k) seg[k] = trow[k];
-#pragma unroll
-    for (int dx = 0; dx < S; ++dx) {
-      const double w = sw[dy * S + dx];
-      if (DENSE || w != 0.0) {  // DENSE: the host checked that no weight is 0
-#pragma unroll
-        for (int j = 0; j < kPx; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(w, seg[j + dx]));
-      }
-    }
-  }
-  OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
-#pragma unroll
-  for (int j = 0; j < kPx; ++j)
-    if (x0 + px + j < W) o[j] = (OUT)acc[j];
-}
-
 // NR output rows per thread (32·NR x 64 tile, 256 threads): each input row
 // segment loaded from smem feeds all NR rows (tap row dy = iy - k for the
 // thread's k-th row), cutting segment and weight loads per output by NR and
@@ -90,13 +42,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // latency.  Tap order per output pixel is still row-major (iy increases), so
 // the result is bit-identical.
 //
-// V2 (default): the row segments come in as 16-byte shared loads, and lane l
+// The row segments come in as 16-byte shared loads, and lane l
 // of a warp takes row group l % 4, pixel group l / 4, so the 8 lanes of each
 // quarter-warp hit 8 distinct 16-byte bank slots (the row stride NR·TW is
 // ≡ 2·odd mod 16 doubles) — conflict-free, where the row-major lane order
 // put 4 lanes on each slot (ncu: 61 % of the shared wavefronts were
 // conflicts).  Same pixels per thread, same tap order.
-template <int R, typename IN, typename OUT, bool DENSE, int MINB, int NR, bool V2 = true>
+template <int R, typename IN, typename OUT, bool DENSE, int MINB, int NR>
 __global__ void __launch_bounds__(kThreads, MINB)
     conv_rows_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
                      const double* __restrict__ weights, OUT* __restrict__ out) {
@@ -120,9 +72,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   __syncthreads();
   static_assert(kTileW / kPx == 8 && kThreads % 32 == 0, "lane mapping assumes 8 pixel groups per row");
   const int lane = tid & 31;
-  const int rgrp = V2 ? (tid >> 5) * 4 + (lane & 3) : tid / (kTileW / kPx);
+  const int rgrp = (tid >> 5) * 4 + (lane & 3);
   const int py = rgrp * NR;  // first of the thread's NR output rows
-  const int px = (V2 ? lane >> 2 : tid % (kTileW / kPx)) * kPx;
+  const int px = (lane >> 2) * kPx;
   const int gy = y0 + py;
   if (gy >= row1) return;
   double acc[NR][kPx];
@@ -134,17 +86,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (int iy = 0; iy < S + NR - 1; ++iy) {  // input rows py .. py+S+NR-2 of the tile
     double seg[kPx + 2 * R];
     const double* trow = tile + (py + iy) * TW + px;
-    if (V2) {
-      static_assert(TW % 2 == 0 && (kPx + 2 * R) % 2 == 0, "16-byte segment loads");
+    static_assert(TW % 2 == 0 && (kPx + 2 * R) % 2 == 0, "16-byte segment loads");
 #pragma unroll
-      for (int q = 0; q < (kPx + 2 * R) / 2; ++q) {
-        const double2 v = reinterpret_cast<const double2*>(trow)[q];
-        seg[2 * q] = v.x;
-        seg[2 * q + 1] = v.y;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < kPx + 2 * R; ++q) seg[q] = trow[q];
+    for (int q = 0; q < (kPx + 2 * R) / 2; ++q) {
+      const double2 v = reinterpret_cast<const double2*>(trow)[q];
+      seg[2 * q] = v.x;
+      seg[2 * q + 1] = v.y;
     }
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -171,87 +118,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
-// Persistent variant (HB_CONV_CFG=1; measured slower than one CTA per tile
-// at 3 CTAs/SM, kept for the record): 2 CTAs per SM walk the tiles
-// round-robin; the halo of the next tile is loaded into registers before the
-// current tile is filtered and stored to the other smem buffer afterwards,
-// so halo load latency hides behind the fp64 work.
-template <int R, typename IN, typename OUT>
-__global__ void __launch_bounds__(kThreads, 2)
-    conv_persist_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
-                        const double* __restrict__ weights, OUT* __restrict__ out, int tiles_x, int ntiles) {
-  constexpr int S = 2 * R + 1;
-  constexpr int TH = kTileH + 2 * R, TW = kTileW + 2 * R;
-  constexpr int HALO = TH * TW;
-  constexpr int PER = (HALO + kThreads - 1) / kThreads;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* sw = reinterpret_cast<double*>(smem);  // [S*S]
-  double* tiles = sw + S * S;                    // [2][TH][TW]
-  const int tid = threadIdx.x;
-  for (int i = tid; i < S * S; i += kThreads) sw[i] = weights[i];
-  IN pre[PER];
-  auto fetch = [&](int t) {
-    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + u * kThreads;
-      if (i < HALO) {
-        const int ty = i / TW, tx = i - ty * TW;
-        const int gy = min(max(y0 - R + ty, 0), H - 1);
-        const int gx = min(max(x0 - R + tx, 0), W - 1);
-        pre[u] = img[(int64_t)gy * W + gx];
-      }
-    }
-  };
-  auto stash = [&](double* buf) {
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + u * kThreads;
-      if (i < HALO) buf[i] = to_f64(pre[u]);
-    }
-  };
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
-  fetch(t);
-  stash(tiles);
-  __syncthreads();
-  const int py = tid / (kTileW / kPx);
-  const int px = (tid % (kTileW / kPx)) * kPx;
-  for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) fetch(tn);
-    const double* tile = tiles + b * HALO;
-    const int y0 = row0 + (t / tiles_x) * kTileH, x0 = (t % tiles_x) * kTileW;
-    const int gy = y0 + py;
-    if (gy < row1) {
-      double acc[kPx];
-#pragma unroll
-      for (int j = 0; j < kPx; ++j) acc[j] = 0.0;
-#pragma unroll 1
-      for (int dy = 0; dy < S; ++dy) {
-        double seg[kPx + 2 * R];
-        const double* trow = tile + (py + dy) * TW + px;
-#pragma unroll
-        for (int k = 0; k < kPx + 2 * R; ++k) seg[k] = trow[k];
-#pragma unroll
-        for (int dx = 0; dx < S; ++dx) {
-          const double w = sw[dy * S + dx];
-          if (w != 0.0) {
-#pragma unroll
-            for (int j = 0; j < kPx; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(w, seg[j + dx]));
-          }
-        }
-      }
-      OUT* o = out + (int64_t)(gy - row0) * W + x0 + px;
-#pragma unroll
-      for (int j = 0; j < kPx; ++j)
-        if (x0 + px + j < W) o[j] = (OUT)acc[j];
-    }
-    if (tn < ntiles) stash(tiles + (b ^ 1) * HALO);
-    __syncthreads();
-  }
-}
-
 // radius > kMaxR: same arithmetic, neighbours read from global memory
 template <typename IN, typename OUT>
 __global__ void conv_generic_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1, int R,
@@ -274,54 +140,21 @@ __global__ void conv_generic_kernel(const IN* __restrict__ img, int H, int W, in
   }
 }
 
+// NR = 3 output rows per thread (96 x 64 tiles), 2 CTAs/SM (measured at
+// r=7: 38 Gpix/s; 2 rows 0.68, 1 row 0.61 of the fp64 peak)
 template <int R, typename IN, typename OUT>
 int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w, bool dense, OUT* out,
                 cudaStream_t s) {
-  constexpr int S = 2 * R + 1;
-  static const int variant = [] {
-    const char* e = getenv("HB_CONV_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  if (variant == 1) {
-    const size_t smem = (size_t)S * S * 8 + 2 * (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 8;
-    HB_CUDA_TRY(cudaFuncSetAttribute(conv_persist_kernel<R, IN, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DeviceInfo di;
-    HB_TRY(device_info(&di));
-    const int tiles_x = (int)ceil_div(W, kTileW);
-    const int64_t ntiles = (int64_t)tiles_x * ceil_div(row1 - row0, kTileH);
-    HB_CHECK_ARG(ntiles < INT32_MAX, "image too large");
-    int64_t grid = (int64_t)di.sms * 2;
-    if (grid > ntiles) grid = ntiles;
-    conv_persist_kernel<R, IN, OUT><<<(unsigned)grid, kThreads, smem, s>>>(img, H, W, row0, row1, w, out, tiles_x, (int)ntiles);
-    return check_launch();
-  }
-  const size_t smem = (size_t)S * S * 8 + (size_t)(kTileH + 2 * R) * (kTileW + 2 * R) * 8;
-  dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH));
+  constexpr int S = 2 * R + 1, NR = 3;
+  const size_t smem = (size_t)((S * S + 1) & ~1) * 8 + (size_t)(kTileH * NR + 2 * R) * (kTileW + 2 * R) * 8;
+  dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH * NR));
   auto launch = [&](auto kern) -> int {
     HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, kThreads, smem, s>>>(img, H, W, row0, row1, w, out);
     return check_launch();
   };
-  // default: NR = 3 output rows per thread, 2 CTAs/SM (measured at r=7:
-  // 31.1 Gpix/s vs 27.9 for NR = 2 and 24.8 for one row); HB_CONV_CFG 2/3/4:
-  // one row per thread, 5-7 other shapes, 8 the row-major lane order
-  if (variant == 0 || (variant >= 5 && variant <= 7)) {
-    auto launch_n = [&](auto kern, int nr) -> int {
-      const size_t smem2 = (size_t)((S * S + 1) & ~1) * 8 + (size_t)(kTileH * nr + 2 * R) * (kTileW + 2 * R) * 8;
-      dim3 grid2((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH * nr));
-      HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      kern<<<grid2, kThreads, smem2, s>>>(img, H, W, row0, row1, w, out);
-      return check_launch();
-    };
-    if (variant == 5) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 2, 2>, 2) : launch_n(conv_rows_kernel<R, IN, OUT, false, 2, 2>, 2);
-    if (variant == 6) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 1, 4>, 4) : launch_n(conv_rows_kernel<R, IN, OUT, false, 1, 4>, 4);
-    if (variant == 7) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 3, 2>, 2) : launch_n(conv_rows_kernel<R, IN, OUT, false, 3, 2>, 2);
-    if (variant == 8) return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 2, 3, false>, 3) : launch_n(conv_rows_kernel<R, IN, OUT, false, 2, 3, false>, 3);
-    return dense ? launch_n(conv_rows_kernel<R, IN, OUT, true, 2, 3>, 3) : launch_n(conv_rows_kernel<R, IN, OUT, false, 2, 3>, 3);
-  }
-  if (variant == 2) return dense ? launch(conv_tile_kernel<R, IN, OUT, true, 2>) : launch(conv_tile_kernel<R, IN, OUT, false, 2>);
-  if (variant == 3) return launch(conv_tile_kernel<R, IN, OUT, false, 3>);
-  return dense ? launch(conv_tile_kernel<R, IN, OUT, true, 3>) : launch(conv_tile_kernel<R, IN, OUT, false, 3>);  // 4: one row, 3 CTAs/SM
+  // all-non-zero weights: the branch-free variant; otherwise zero taps are skipped like the reference
+  return dense ? launch(conv_rows_kernel<R, IN, OUT, true, 2, NR>) : launch(conv_rows_kernel<R, IN, OUT, false, 2, NR>);
 }
 
 template <typename IN, typename OUT>

@@ -259,15 +259,9 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     HB_TRY(alloc(&L->len, (size_t)L->nsub * 8, s));
     int64_t blocks = ceil_div(L->nsub, 128 * kChains);
     if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;  // 2048 resident threads / SM
-    static const int lr_cfg = [] {
-      const char* e = getenv("HB_LR_CFG");
-      return e ? atoi(e) : 0;
-    }();
-    DevBuf jobs;
-    if (lr_cfg != 2) {  // dynamic sublist claiming (default; +1 %: 12.62 vs 12.49 Gnodes/s); 2: static stride
-      HB_TRY(alloc(&jobs, 8, s));
-      HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
-    }
+    DevBuf jobs;  // dynamic sublist claiming (+1 % over a static stride: 12.62 vs 12.49 Gnodes/s)
+    HB_TRY(alloc(&jobs, 8, s));
+    HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
     if (first && w0 != nullptr) {
       lr_walk_kernel<S, true><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, w0, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),

@@ -456,14 +456,6 @@ __global__ void csr_validate_kernel(const P* __restrict__ row_ptr, const C* __re
 
 int idx_size_ok(int code) { return code == HB_I32 || code == HB_I64; }
 
-int spmv_variant() {
-  static int v = [] {
-    const char* e = getenv("HB_SPMV_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 // Shared-memory carveout: just what the resident CTAs need.  The rest of the
 // unified 256 KB stays L1, which holds the in-flight x gathers — with less
 // than ~100 KB of L1 the SM's gather rate halves (scripts/micro/l2gather.cu:
@@ -490,9 +482,8 @@ int launch_lpr(const void* rp, const void* ci, const double* v, const double* x,
   return check_launch();
 }
 
-// HB_SPMV_CFG (experiments, scripts/sweep_spmv.sh): 0 default, 1 the generic
-// CTA-blocked kernel, 2.. alternative lane-per-row shapes <CW, S, WARPS, MINB, B>
-// (7/8: 6 or 8 gathers in flight per lane, 9: 3 stages — 84-88 us vs 83 us).
+// Lane-per-row tiles: 256-nnz smem chunks, 2 stages, 4 warps per CTA, 6 CTAs/SM,
+// 4 gathers in flight per lane (measured best of the shapes tried).
 template <typename P, typename C, typename Q>
 int launch_spmv(const void* rp, const void* ci, const double* v, const double* x, int64_t row0,
                 int64_t row1, const void* pm, double* y, int mode, cudaStream_t s) {
@@ -503,7 +494,6 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
   auto p = reinterpret_cast<const P*>(rp);
   auto c = reinterpret_cast<const C*>(ci);
   auto q = reinterpret_cast<const Q*>(pm);
-  const int var = spmv_variant();
   if (mode == 2) {
     // nnz of the range is needed for the grid: one small D2H read of row_ptr[row0], row_ptr[row1]
     P ends[2];
@@ -530,19 +520,7 @@ int launch_spmv(const void* rp, const void* ci, const double* v, const double* x
     spmv_warp_kernel<P, C, Q><<<(int)blocks, 256, 0, s>>>(p, c, v, x, row0, row1, q, y);
     return check_launch();
   }
-  if (sizeof(P) == 4 && sizeof(C) == 4 && var != 1) {
-    switch (var) {
-      case 2: return launch_lpr<Q, 256, 2, 4, 4, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 3: return launch_lpr<Q, 256, 2, 8, 3, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 4: return launch_lpr<Q, 256, 2, 4, 6, 3>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 5: return launch_lpr<Q, 256, 2, 4, 4, 8>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 6: return launch_lpr<Q, 192, 2, 4, 8, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 7: return launch_lpr<Q, 256, 2, 4, 6, 6>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 8: return launch_lpr<Q, 256, 2, 4, 6, 8>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      case 9: return launch_lpr<Q, 256, 3, 4, 5, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
-      default: return launch_lpr<Q, 256, 2, 4, 6, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
-    }
-  }
+  if (sizeof(P) == 4 && sizeof(C) == 4) return launch_lpr<Q, 256, 2, 4, 6, 4>(rp, ci, v, x, row0, row1, pm, y, di, s);
   const int64_t blocks = ceil_div(rows, kRows);
   if (blocks > INT32_MAX) { set_error("too many rows"); return HB_EINVAL; }
   spmv_seq_kernel<P, C, Q><<<(unsigned)blocks, kRows, 0, s>>>(p, c, v, x, row0, row1, q, y);
@@ -860,8 +838,9 @@ int preprocess_impl(const void* rp, const void* col, const double* val, int64_t 
   row_len_kernel<PI><<<(int)g, 256, 0, s>>>((const PI*)rp, rows, len.as<uint32_t>(), idx.as<uint32_t>());
   HB_TRY(check_launch());
   int32_t passes = 0;
+  // stable argsort: the ballot ranking (its stability is by construction)
   HB_TRY(hb_sort(len.ptr, len.ptr, HB_U32, idx.as<uint32_t>(), idx.as<uint32_t>(), rows, &passes,
-                 HB_DEVICE_PTRS | HB_ASYNC, s));
+                 HB_DEVICE_PTRS | HB_ASYNC | HB_SORT_BALLOT, s));
   const int64_t nb = ceil_div(rows, kScanTile);
   DevBuf sums;
   HB_TRY(alloc(&sums, (size_t)(nb + 1) * 8, s));

@@ -218,8 +218,9 @@ def device_gen_list(n: int, seed: int, succ_dtype=np.int32):
     device_splitmix(draws, seed, _lib.HB_GEN_RAW)
     order = torch.arange(n, dtype=torch.int32, device="cuda")
     st = current_stream_handle(draws)
+    # stable argsort: the ballot ranking (stable by construction)
     _lib.call("hb_sort", vp(draws.data_ptr()), vp(draws.data_ptr()), _lib.DTYPE_CODES["u8"], vp(order.data_ptr()),
-              vp(order.data_ptr()), n, None, _lib.HB_DEVICE_PTRS, st)
+              vp(order.data_ptr()), n, None, _lib.HB_DEVICE_PTRS | _lib.HB_SORT_BALLOT, st)
     del draws
     tdt = torch.int32 if np.dtype(succ_dtype) == np.int32 else torch.int64
     succ = torch.empty(n, dtype=tdt, device="cuda")

@@ -233,10 +233,13 @@ SORT_MAX_DEPTH = 8
 _SORT_CODES = {np.dtype(np.uint32): 5, np.dtype(np.int32): 6, np.dtype(np.uint64): 7, np.dtype(np.int64): 8}
 
 
-def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False) -> tuple[Any, Any, int]:
+def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False,
+             ballot: bool = False) -> tuple[Any, Any, int]:
     """LSD radix sort on the GPU (hb_sort).  CUDA tensors are sorted in place
     (payload permuted alongside, stably); host arrays are left untouched and
-    sorted copies returned.  Returns (keys, payload, digit passes executed)."""
+    sorted copies returned.  Returns (keys, payload, digit passes executed).
+    `ballot` ranks with the ballot multi-split instead of the (device-checked)
+    lane-ordered shared atomics."""
     import ctypes
 
     _lib.load()
@@ -251,7 +254,7 @@ def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False) -> t
         vb = buf(payload) if is_device_array(payload) else buf(payload, np.uint32)
         if vb.dtype not in (np.dtype(np.uint32), np.dtype(np.int32)) or vb.size != kb.size:
             raise TypeError("payload must be uint32 (or non-negative int32) with one entry per key")
-    flags = flags_for(kb, *([vb] if vb else []), asynchronous=asynchronous)
+    flags = flags_for(kb, *([vb] if vb else []), asynchronous=asynchronous) | (_lib.HB_SORT_BALLOT if ballot else 0)
     if kb.device:
         k_out, v_out = kb.ptr, (vb.ptr if vb else 0)
         res_k, res_v = keys, payload

@@ -112,3 +112,40 @@ def test_split_points_kernel():
     want = host_split_points(*(torch.from_numpy(a) for a in (keys, idx, pk, pi)))
     got = gpu_split_points(*(torch.from_numpy(a).cuda() for a in (keys, idx, pk, pi)))
     assert want.tolist() == got.cpu().tolist()
+
+
+@pytest.mark.parametrize("ballot", [False, True])
+@pytest.mark.parametrize("dtype", [np.uint32, np.int32, np.uint64, np.int64])
+def test_stable_payload_adversarial_duplicates(ballot, dtype):
+    """The production ranking (lane-ordered shared atomics, device-checked)
+    and the ballot multi-split both give the stable argsort on inputs built
+    to stress the ranking: all-equal, two values alternating, runs of 32
+    equal keys per warp, one hot digit among random keys, and every digit
+    position constant but one."""
+    from oracle import sort as osort
+    from paper_1303_2171_b200.kernels_regular import gpu_sort
+
+    rs = np.random.default_rng(11)
+    n = 3_000_017
+    cases = {
+        "all_equal": np.full(n, 7, dtype=np.int64),
+        "alternating": np.arange(n) % 2,
+        "warp_runs": (np.arange(n) // 32) % 5,
+        "hot_digit": np.where(rs.random(n) < 0.9, 42, rs.integers(0, 1 << 30, n)),
+        "one_live_digit": (rs.integers(0, 256, n) << 16) | 0x1234,
+        "few_values": rs.integers(0, 3, n),
+    }
+    for name, raw in cases.items():
+        keys = raw.astype(dtype)
+        pay = np.arange(n, dtype=np.uint32)
+        k, v, _ = gpu_sort(keys, pay, ballot=ballot)
+        assert np.array_equal(k, np.sort(keys, kind="stable")), name
+        assert osort.check_stable_payload(keys, k, v), name
+        import torch
+
+        kt = torch.from_numpy(keys.view(np.int64 if keys.itemsize == 8 else np.int32)).cuda()
+        kt = kt.view(getattr(torch, np.dtype(dtype).name))
+        vt = torch.arange(n, dtype=torch.int32, device="cuda")
+        gpu_sort(kt, vt, ballot=ballot)  # device-resident, in place
+        got_v = vt.cpu().numpy().astype(np.uint32)
+        assert np.array_equal(got_v, v), name

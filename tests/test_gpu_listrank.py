@@ -147,3 +147,29 @@ def test_stats_large_list_device():
     _, (rounds, sizes, reduced, removed, subl) = olr.list_rank_with_stats(succ, head, 7)
     assert (st.fis_rounds, st.round_sizes, st.reduced_size, st.removed_total, st.sublist_count) == (
         rounds, sizes, reduced, removed, subl)
+
+
+@pytest.mark.parametrize("order", ["identity", "reverse", "random", "blocks"])
+@pytest.mark.parametrize("n", [(1 << 20), (1 << 20) + 37, 3_000_001])
+def test_logged_walk_orders(n, order):
+    """Lists of >= 2^20 nodes take the logged level-1 walk (sequential
+    (node, offset) log + bucketed scatter of the ranks): every ordering,
+    heads on and off the 64-node grid, sizes not a power of two."""
+    rs = np.random.default_rng(n)
+    if order == "identity":
+        seq = np.arange(n)
+    elif order == "reverse":
+        seq = np.arange(n)[::-1].copy()
+    elif order == "random":
+        seq = rs.permutation(n)
+    else:  # long runs of consecutive nodes in random block order
+        blk = 1000
+        starts = rs.permutation((n + blk - 1) // blk) * blk
+        seq = np.concatenate([np.arange(s0, min(n, s0 + blk)) for s0 in starts])
+    succ = np.full(n, -1, dtype=np.int64)
+    succ[seq[:-1]] = seq[1:]
+    head = int(seq[0])
+    want = np.empty(n, dtype=np.int64)
+    want[seq] = np.arange(n)
+    got = gpu_list_rank(succ.astype(np.int32), head)
+    assert np.array_equal(got, want), (n, order)

@@ -50,8 +50,7 @@ FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
 DETAIL_FILE = ROOT / "gpurun_out" / "bench_detail.json"
 
-RANDOM_READ_PEAK = 51.5   # G random 4-B DRAM reads/s, scripts/micro/gather.cu
-RANDOM_WRITE_PEAK = 24.8  # G random 8-B DRAM writes/s (read-fill + write), same micro
+RANDOM_READ_PEAK = 42.2   # G dependent random 4-B reads/s (~118 B of HBM each), scripts/micro/rand_read.cu
 FP64_PEAK_GFLOPS = 18370.0  # non-FMA fp64 instructions/s, scripts/micro/fp64peak.cu
 METRIC = "per-workload throughput (SpMV GFLOP/s, sort Mkeys/s) and HBM-roofline fraction"
 
@@ -784,12 +783,17 @@ class LrBench(Bench):
     def bytes_per_launch(self):
         return 12 * self.n // self.world
 
+    SEQ_BYTES_PER_NODE = 106  # log 8 + pairs 16 + node sort ~70 (1.03 n entries) + widen 12
+
     def roofline_extra(self, ms):
-        # random-access bound: t >= reads/R + writes/W (measured rates)
-        reads = writes = self.n // self.world
-        bound_ms = (reads / RANDOM_READ_PEAK + writes / RANDOM_WRITE_PEAK) / 1e9 * 1e3
+        # t >= one dependent random successor read per node at the measured
+        # rate + the sequential passes (log, pairs, node sort, widen) at HBM peak
+        n = self.n // self.world
+        peak, _ = hbm_peak()
+        bound_ms = (n / RANDOM_READ_PEAK / 1e9 + n * self.SEQ_BYTES_PER_NODE / (peak * 1e9)) * 1e3
         return {"random_access": {"bound_ms": bound_ms, "frac": bound_ms / ms,
-                                  "peak_read_g_per_s": RANDOM_READ_PEAK, "peak_write_g_per_s": RANDOM_WRITE_PEAK}}
+                                  "peak_read_g_per_s": RANDOM_READ_PEAK,
+                                  "seq_bytes_per_node": self.SEQ_BYTES_PER_NODE}}
 
     def verify(self):
         if self.world > 1:
@@ -932,7 +936,8 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
 
     # end to end through the public API (host buffers)
     wl.e2e_setup()
-    wl.e2e_step()
+    for _ in range(args.warmup):  # untimed: device memory pools and pinned stages settle
+        wl.e2e_step()
     torch.cuda.synchronize()
     barrier(world)
     e_steps = max(1, min(args.steps, args.e2e_steps))

@@ -154,20 +154,19 @@ __global__ void __launch_bounds__(128)
 
 // ---------------------------------------------------------------- level-0 log walk
 // The level-0 walk of the plain path writes (sublist, offset) to a RANDOM
-// node slot per node: a random 8-byte store costs a DRAM read-fill plus a
-// write-back (24.8 G/s measured, two thirds of the walk's time).  The log
-// walk instead appends (node, offset) to per-thread 32-entry chunks of a
-// sequential log (chunk ids from one counter; each chunk opens with a
-// marker holding its sublist id, and every walk start writes a marker), and
-// counts the nodes per rank-window bucket (node >> bshift, <= 64 buckets).
-// After the sublist chain is ranked, lr_bucket_kernel turns log entries into
-// (node, rank) pairs grouped by bucket, and lr_scatter_kernel writes rank[]
-// bucket by bucket: each bucket's rank window (<= 32 MB) is written while it
-// sits in L2, so the scattered 8-byte stores leave the chip as full sectors.
+// node slot per node.  On B200 a scattered 8-byte store costs a sector
+// read-modify-write in DRAM (HBM3e has no write mask) and the L2 does not
+// merge separate partial stores to one sector, however local they are
+// (profiles/micro_scatter_window_r02.txt): ~55 B of DRAM traffic per node.
+// The log walk instead appends (node, offset) to per-thread 32-entry chunks
+// of a sequential log (chunk ids from one counter; each chunk opens with a
+// marker holding its sublist id, and every walk start writes a marker).
+// After the sublist chain is ranked, the log becomes (node, rank) pairs
+// (lr_log_pairs_kernel), which the library's radix sort orders by node —
+// coalesced passes — and the ranks are widened into rank[] in node order.
 constexpr int kLogChunk = 32;
 constexpr uint32_t kMarkBit = 0x80000000u;
 constexpr uint32_t kEmptyHi = 0xffffffffu;
-constexpr int kMaxBuckets = 64;
 constexpr int64_t kLogMin = 1 << 20;  // smaller lists: the plain walk (everything fits in L2)
 
 template <typename S>
@@ -175,13 +174,31 @@ __global__ void __launch_bounds__(128)
     lr_walk_log_kernel(const S* __restrict__ succ, int64_t n, int64_t head, int64_t nsub, int64_t extra,
                        uint64_t* __restrict__ log, unsigned long long* __restrict__ chunk_ctr, int64_t max_chunks,
                        int64_t* __restrict__ nxt, int64_t* __restrict__ len, unsigned long long* __restrict__ err,
-                       unsigned long long* __restrict__ jobs, int bshift, unsigned long long* __restrict__ bucket_count) {
-  __shared__ unsigned int hist[kMaxBuckets];
-  for (int i = threadIdx.x; i < kMaxBuckets; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
+                       unsigned long long* __restrict__ jobs) {
+  // Entries are held back in registers and stored 4 at a time (one full
+  // 32-byte sector as two 16-byte stores issued together): a sector filled
+  // entry by entry over microseconds would be evicted part-written and cost
+  // a DRAM read-modify-write (no write mask on HBM3e).  Chunks are 256-byte
+  // aligned, so every group of 4 slots is one sector.
   int64_t cbase = 0;
   int fill = kLogChunk;  // no chunk yet
   bool overflow = false;
+  uint64_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+  int nb = 0;
+  auto push = [&](uint64_t e) {  // next slot of the current chunk
+    if (nb == 0) b0 = e;
+    else if (nb == 1) b1 = e;
+    else if (nb == 2) b2 = e;
+    else b3 = e;
+    ++nb;
+    ++fill;
+    if (nb == 4) {
+      uint64_t* p = log + cbase + fill - 4;
+      asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(b0), "l"(b1) : "memory");
+      asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p + 2), "l"(b2), "l"(b3) : "memory");
+      nb = 0;
+    }
+  };
   auto put = [&](uint64_t e, uint32_t j) {
     if (fill == kLogChunk) {
       const int64_t c = (int64_t)atomicAdd(chunk_ctr, 1ull);
@@ -190,11 +207,10 @@ __global__ void __launch_bounds__(128)
         return;
       }
       cbase = c * kLogChunk;
-      st_stream(log + cbase, (uint64_t)(kMarkBit | j) << 32);
-      fill = 1;
+      fill = 0;
+      push((uint64_t)(kMarkBit | j) << 32);
     }
-    st_stream(log + cbase + fill, e);
-    ++fill;
+    push(e);
   };
   for (;;) {
     const int64_t jj = (int64_t)atomicAdd(jobs, 1ull);
@@ -206,17 +222,12 @@ __global__ void __launch_bounds__(128)
       continue;
     }
     const uint32_t j = (uint32_t)jj;
-    if (fill < kLogChunk && fill > 0) {  // a new walk inside the current chunk: its marker
-      st_stream(log + cbase + fill, (uint64_t)(kMarkBit | j) << 32);
-      ++fill;
-    }
+    if (fill < kLogChunk && fill > 0) push((uint64_t)(kMarkBit | j) << 32);  // a new walk inside the chunk: its marker
     put((uint64_t)h << 32, j);
-    atomicAdd(&hist[h >> bshift], 1u);
     int64_t acc = 1, steps = 0;
     int64_t v = ld_succ(succ + h);
     while (v != -1 && !is_head(v, head) && steps <= n) {
       put(((uint64_t)v << 32) | (uint64_t)(uint32_t)acc, j);
-      atomicAdd(&hist[v >> bshift], 1u);
       ++acc;
       ++steps;
       v = ld_succ(succ + v);
@@ -226,80 +237,36 @@ __global__ void __launch_bounds__(128)
     len[jj] = steps > n ? n + 1 : acc;
   }
   if (overflow) atomicAdd(err, 1ull);
-  if (fill < kLogChunk && fill > 0)
-    for (int f = fill; f < kLogChunk; ++f) st_stream(log + cbase + f, (uint64_t)kEmptyHi << 32);
-  __syncthreads();
-  for (int i = threadIdx.x; i < kMaxBuckets; i += blockDim.x)
-    if (hist[i]) atomicAdd(bucket_count + i, (unsigned long long)hist[i]);
+  if (!overflow)
+    while (fill > 0 && fill < kLogChunk) push((uint64_t)kEmptyHi << 32);  // pad (and flush) the last chunk
 }
 
-// bucket starts: cursor[b] = sum of counts below b (one warp, <= 64 buckets)
-__global__ void lr_bucket_scan_kernel(const unsigned long long* __restrict__ count, unsigned long long* __restrict__ cursor) {
-  if (threadIdx.x == 0) {
-    unsigned long long run = 0;
-    for (int b = 0; b < kMaxBuckets; ++b) {
-      cursor[b] = run;
-      run += count[b];
-    }
-  }
-}
-
-// log entries → (rank << 32 | node) grouped by bucket; rank = prefix[sublist] + offset
-// 16 warps x 2 chunks = 1024 entries per CTA round; within a round, slots per
-// bucket come from shared atomics, the bucket's run is reserved with one
-// global atomic, so each bucket receives a contiguous run per round.
-__global__ void __launch_bounds__(512)
-    lr_bucket_kernel(const uint64_t* __restrict__ log, const unsigned long long* __restrict__ chunk_ctr,
-                     int64_t max_chunks, const int64_t* __restrict__ prefix, int bshift,
-                     unsigned long long* __restrict__ cursor, uint64_t* __restrict__ part) {
-  __shared__ unsigned int cnt[kMaxBuckets];
-  __shared__ unsigned long long base[kMaxBuckets];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t nchunks = (int64_t)*chunk_ctr;
-  if (nchunks > max_chunks) nchunks = max_chunks;
+// log slot → (key = node, val = prefix[sublist] + offset); markers and
+// padding → key 0xffffffff (sorted behind every node)
+__global__ void lr_log_pairs_kernel(const uint64_t* __restrict__ log, int64_t slots, const int64_t* __restrict__ prefix,
+                                    uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
   const uint32_t le = (2u << lane) - 1u;  // lanes <= me
-  for (int64_t g = (int64_t)blockIdx.x * 32; g < nchunks; g += (int64_t)gridDim.x * 32) {
-    if (threadIdx.x < kMaxBuckets) cnt[threadIdx.x] = 0;
-    __syncthreads();
-    uint64_t out[2];
-    int bk[2];
-    unsigned int slot[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int64_t c = g + warp * 2 + k;
-      bk[k] = -1;
-      if (c >= nchunks) continue;
-      const uint64_t e = log[c * kLogChunk + lane];
-      const uint32_t hi = (uint32_t)(e >> 32);
-      const bool mark = (hi & kMarkBit) && hi != kEmptyHi;
-      const uint32_t mb = __ballot_sync(0xffffffffu, mark);
-      const int src = 31 - __clz(mb & le);  // lane 0 always holds the chunk's marker
-      const uint32_t j = __shfl_sync(0xffffffffu, hi & ~kMarkBit, src);
-      if (!(hi & kMarkBit)) {
-        const int64_t r = prefix[j] + (int64_t)(uint32_t)e;
-        out[k] = ((uint64_t)r << 32) | hi;
-        bk[k] = (int)(hi >> bshift);
-        slot[k] = atomicAdd(&cnt[bk[k]], 1u);
-      }
+  // warps cover whole chunks (32 slots): blockDim is a multiple of 32, slots of kLogChunk
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = i < slots ? __ldcs(reinterpret_cast<const unsigned long long*>(log) + i) : ((uint64_t)kEmptyHi << 32);
+    const uint32_t hi = (uint32_t)(e >> 32);
+    const bool mark = (hi & kMarkBit) && hi != kEmptyHi;
+    const uint32_t mb = __ballot_sync(0xffffffffu, mark);
+    const int src = 31 - __clz(mb & le);
+    const uint32_t j = __shfl_sync(0xffffffffu, hi & ~kMarkBit, src < 0 ? 0 : src);
+    if (i < slots) {
+      const bool node = !(hi & kMarkBit);
+      key[i] = node ? hi : 0xffffffffu;
+      val[i] = node ? (uint32_t)(prefix[j] + (int64_t)(uint32_t)e) : 0u;
     }
-    __syncthreads();
-    if (threadIdx.x < kMaxBuckets && cnt[threadIdx.x])
-      base[threadIdx.x] = atomicAdd(cursor + threadIdx.x, (unsigned long long)cnt[threadIdx.x]);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (bk[k] >= 0) part[base[bk[k]] + slot[k]] = out[k];
-    __syncthreads();
   }
 }
 
-// rank[node] = rank, in bucket order (the CTAs in flight cover one or two
-// buckets: their rank windows stay L2-resident until fully written)
-__global__ void lr_scatter_kernel(const uint64_t* __restrict__ part, int64_t n, int64_t* __restrict__ rank) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = part[i];
-    rank[(uint32_t)e] = (int64_t)(e >> 32);
-  }
+__global__ void lr_widen_kernel(const uint32_t* __restrict__ val, int64_t n, int64_t* __restrict__ rank) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    rank[i] = (int64_t)val[i];
 }
 
 // rank[v] = prefix[sublist] + local
@@ -366,9 +333,8 @@ struct Level {
   int64_t n = 0, nsub = 0, extra = -1, head = 0;
   // level 0 with the log walk
   bool logged = false;
-  DevBuf log, ctr, bcount;
+  DevBuf log, ctr, key, val;
   int64_t max_chunks = 0;
-  int bshift = 0;
 };
 
 // Rank the list `succ` (n nodes, first node `head`): out_rank[v] = sum of the
@@ -404,18 +370,17 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     const int64_t regular = ceil_div(cur_n, kK);
     L->extra = (cur_head % kK == 0) ? -1 : regular;
     L->nsub = regular + (L->extra >= 0 ? 1 : 0);
-    L->logged = first && w0 == nullptr && cur_n >= kLogMin && cur_n < (1ll << 31);
+    L->logged = first && w0 == nullptr && cur_n >= kLogMin && cur_n <= (1ll << 29);  // sort size < 2^30
     if (L->logged) {
-      int bits = 0;
-      while ((1ll << bits) < cur_n) ++bits;
-      L->bshift = bits > 6 ? bits - 6 : 0;  // <= 64 rank windows
       // every full chunk holds >= 31 node / walk-start entries; plus one partial chunk per thread
       L->max_chunks = (cur_n + L->nsub) / (kLogChunk - 1) + (int64_t)di.sms * 16 * 128 + 64;
+      // log + (node, rank) pair arrays allocated together, up front: the same
+      // allocation pattern every call keeps the stream-ordered pool from growing
       HB_TRY(alloc(&L->log, (size_t)L->max_chunks * kLogChunk * 8, s));
+      HB_TRY(alloc(&L->key, (size_t)L->max_chunks * kLogChunk * 4, s));
+      HB_TRY(alloc(&L->val, (size_t)L->max_chunks * kLogChunk * 4, s));
       HB_TRY(alloc(&L->ctr, 8, s));
-      HB_TRY(alloc(&L->bcount, kMaxBuckets * 8, s));
       HB_CUDA_TRY(cudaMemsetAsync(L->ctr.ptr, 0, 8, s));
-      HB_CUDA_TRY(cudaMemsetAsync(L->bcount.ptr, 0, kMaxBuckets * 8, s));
     } else if (first) {
       L->tmp.ptr = out_rank;  // packed (sublist, offset) lives in the output until expanded
       L->tmp.owned = false;
@@ -433,7 +398,7 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       lr_walk_log_kernel<S><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, cur_n, cur_head, L->nsub, L->extra, L->log.as<uint64_t>(),
           L->ctr.as<unsigned long long>(), L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),
-          err.as<unsigned long long>(), jobs.as<unsigned long long>(), L->bshift, L->bcount.as<unsigned long long>());
+          err.as<unsigned long long>(), jobs.as<unsigned long long>());
     } else if (first && w0 != nullptr) {
       lr_walk_kernel<S, true><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, w0, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
@@ -516,16 +481,24 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       dst = L->ranked.as<int64_t>();
     }
     if (L->logged) {
-      DevBuf cursor, part;
-      HB_TRY(alloc(&cursor, kMaxBuckets * 8, s));
-      HB_TRY(alloc(&part, (size_t)L->n * 8, s));
-      lr_bucket_scan_kernel<<<1, 32, 0, s>>>(L->bcount.as<unsigned long long>(), cursor.as<unsigned long long>());
-      lr_bucket_kernel<<<di.sms * 4, 512, 0, s>>>(L->log.as<uint64_t>(), L->ctr.as<unsigned long long>(),
-                                                  L->max_chunks, prefix, L->bshift, cursor.as<unsigned long long>(),
-                                                  part.as<uint64_t>());
-      int64_t sb = ceil_div(L->n, 256);
-      if (sb > (int64_t)di.sms * 8) sb = (int64_t)di.sms * 8;
-      lr_scatter_kernel<<<(int)sb, 256, 0, s>>>(part.as<uint64_t>(), L->n, dst);
+      unsigned long long used = 0;
+      HB_CUDA_TRY(cudaMemcpyAsync(&used, L->ctr.ptr, 8, cudaMemcpyDeviceToHost, s));
+      HB_CUDA_TRY(cudaStreamSynchronize(s));
+      const int64_t slots = (int64_t)used * kLogChunk;
+      DevBuf& key = L->key;
+      DevBuf& val = L->val;
+      int64_t pb = ceil_div(slots, 256);
+      if (pb > (int64_t)di.sms * 16) pb = (int64_t)di.sms * 16;
+      lr_log_pairs_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, key.as<uint32_t>(),
+                                                 val.as<uint32_t>());
+      HB_TRY(check_launch());
+      // order the pairs by node: the first n keys are 0..n-1 (a valid list has
+      // one log entry per node; the chain check above guarantees it)
+      HB_TRY(hb_sort(key.ptr, key.ptr, HB_U32, val.as<uint32_t>(), val.as<uint32_t>(), slots, nullptr,
+                     HB_DEVICE_PTRS | HB_ASYNC, s));
+      int64_t wb = ceil_div(L->n, 256);
+      if (wb > (int64_t)di.sms * 16) wb = (int64_t)di.sms * 16;
+      lr_widen_kernel<<<(int)wb, 256, 0, s>>>(val.as<uint32_t>(), L->n, dst);
       HB_TRY(check_launch());
       prefix = dst;
       continue;

@@ -112,6 +112,20 @@ int hb_spmv_csr(const void* row_ptr, int ptr_code, const void* col_idx, int col_
                 const double* values, int64_t row0, int64_t row1, int64_t cols, const double* x,
                 const void* perm, int perm_code, double* y, int mode, int flags, void* stream);
 
+/* SELL-32 copy of a device int32 CSR (the bit-exact SpMV's conflict-free
+ * layout): tile t = rows [32t, 32t+32) stored column-major, its length the
+ * longest row; tile_off (device, ntiles+1 int64) = element offsets.
+ * hb_spmv_sell_build with sell_col == NULL sizes it (tile_off + *total_out,
+ * host), then with sell_col/sell_val (total entries each) fills it.
+ * hb_spmv_sell = hb_spmv_csr mode HB_SPMV_SEQ on that layout (row_ptr still
+ * gives the row lengths), bit-identical.  Device pointers only.            */
+int hb_spmv_sell_build(const int32_t* row_ptr, const int32_t* col_idx, const double* values, int64_t rows,
+                       int64_t* tile_off, int32_t* sell_col, double* sell_val, int64_t* total_out, int flags,
+                       void* stream);
+int hb_spmv_sell(const int32_t* row_ptr, const int64_t* tile_off, const int32_t* sell_col, const double* sell_val,
+                 int64_t row0, int64_t row1, const double* x, const void* perm, int perm_code, double* y, int flags,
+                 void* stream);
+
 /* CsrMatrix invariants (kernels_irregular.py:44-60) checked on the device:
  * *flags_out |= 1 bad row_ptr ends, 2 decreasing row_ptr, 4 column out of
  * range, 8 columns not strictly increasing within a row.                   */

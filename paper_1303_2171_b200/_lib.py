@@ -60,6 +60,8 @@ _SIGNATURES: dict[str, list] = {
     "hb_link_order": [_vp, _i64, _vp, _int, _int, _vp],
     "hb_list_fis_stats": [_vp, _int, _i64, _i64, _u64, _i32, _vp, _i32, _vp, _int, _vp],
     "hb_gen_csr": [_i64, _i64, _i64, _u64, _u64, _u64, _vp, _int, _vp, _int, _vp, _i64, _vp, _int, _vp],
+    "hb_spmv_sell_build": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _int, _vp],
+    "hb_spmv_sell": [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _int, _vp, _int, _vp],
     "hb_partition_nnz": [_vp, _int, _i64, _i64, _i32, _vp, _int, _vp],
     "hb_scatter_perm": [_vp, _i64, _int, _vp, _int, _vp, _int, _vp],
     "hb_merge_runs": [_vp, _int, _vp, _i64, _vp, _i32, _vp, _vp, _int, _vp],

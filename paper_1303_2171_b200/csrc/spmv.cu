@@ -1053,3 +1053,241 @@ extern "C" int hb_gen_csr(int64_t rows, int64_t cols, int64_t avg, uint64_t seed
   if (rc != HB_OK) return rc;
   return finish(flags, s);
 }
+
+// ------------------------------------------------------------------ SELL-32 layout
+// The lane-per-row kernel reads lane i's row slice at offset a_i + j of a
+// CSR chunk in shared memory; nnz-sorted tiles have equal row lengths L, so
+// the 32 lanes read at a stride of L elements — 8-byte reads conflict
+// 16/gcd(L,16)-ways (ncu: 2.2 M of the 6.4 M shared wavefronts were bank
+// conflicts, all on the L1 data path the x gathers need).  The SELL-32 copy
+// of the matrix stores each 32-row tile column-major (element j of the
+// tile's row i at tile_off[t] + 32 j + i, tile length = its longest row, the
+// padding never read): the stage is still filled by one contiguous bulk copy
+// per chunk, and a warp's reads of step j are 32 consecutive words —
+// conflict-free, 3 wavefronts per 32 nonzeros instead of ~12.  Same per-row
+// sequential fp64 arithmetic (bit-identical).  Built once per device matrix
+// (the nnz-sorted matrix of spmv_preprocess: padding ~0).
+namespace hb {
+namespace {
+
+__global__ void sell_size_kernel(const int32_t* __restrict__ rp, int64_t rows, int64_t* __restrict__ tlen) {
+  const int64_t ntiles = ceil_div(rows, 32);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = 0;
+    const int64_t r1 = min((t + 1) * 32, rows);
+    for (int64_t r = t * 32; r < r1; ++r) m = max(m, (int64_t)rp[r + 1] - (int64_t)rp[r]);
+    tlen[t] = m * 32;
+  }
+}
+
+__global__ void sell_scan_kernel(int64_t* __restrict__ v, int64_t n) {
+  // exclusive scan in place, v[n] = total; one CTA of 1024 threads, blocked
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t a = min((int64_t)tid * per, n), b = min(a + per, n);
+  int64_t s = 0;
+  for (int64_t i = a; i < b; ++i) s += v[i];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t run = 0;
+    for (int k = 0; k < 1024; ++k) {
+      const int64_t c = part[k];
+      part[k] = run;
+      run += c;
+    }
+    v[n] = run;
+  }
+  __syncthreads();
+  int64_t run = part[tid];
+  for (int64_t i = a; i < b; ++i) {
+    const int64_t c = v[i];
+    v[i] = run;
+    run += c;
+  }
+}
+
+__global__ void sell_fill_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const double* __restrict__ val, int64_t rows, const int64_t* __restrict__ toff,
+                                 int32_t* __restrict__ scol, double* __restrict__ sval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t ntiles = ceil_div(rows, 32);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
+    const int64_t r = t * 32 + lane;
+    const int64_t rs = r < rows ? rp[r] : 0, re = r < rows ? rp[r + 1] : 0;
+    const int64_t base = toff[t], len = (toff[t + 1] - base) / 32;
+    for (int64_t j = 0; j < len; ++j) {
+      const bool in = rs + j < re;
+      scol[base + j * 32 + lane] = in ? col[rs + j] : 0;
+      sval[base + j * 32 + lane] = in ? val[rs + j] : 0.0;
+    }
+  }
+}
+
+constexpr int kSellCJ = 8;     // j-steps per stage item (32 x 8 elements: 2 KB vals + 1 KB cols)
+constexpr int kSellS = 2;      // stages per warp
+constexpr int kSellWarps = 4;  // warps per CTA
+constexpr int kSellMinB = 6;   // CTAs per SM
+constexpr int kSellB = 4;      // x gathers in flight per lane per batch
+constexpr size_t kSellStage = (size_t)kSellCJ * 32 * 12;
+constexpr size_t kSellBytes = (size_t)kSellWarps * kSellS * kSellStage;
+
+template <typename Q>
+__global__ void __launch_bounds__(32 * kSellWarps, kSellMinB)
+    spmv_sell_kernel(const int32_t* __restrict__ row_ptr, const int64_t* __restrict__ toff,
+                     const int32_t* __restrict__ scol, const double* __restrict__ sval, const double* __restrict__ x,
+                     int64_t row0, int64_t row1, const Q* __restrict__ perm, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_all[kSellWarps][kSellS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wsm = smem + (size_t)warp * kSellS * kSellStage;
+  uint64_t* full = full_all[warp];
+  auto stv = [&](int s) { return reinterpret_cast<const double*>(wsm + s * kSellStage); };
+  auto stc = [&](int s) { return reinterpret_cast<const int32_t*>(wsm + s * kSellStage + kSellCJ * 32 * 8); };
+  const uint64_t keep = l2_evict_last();
+  const int64_t t0 = row0 / 32, t1 = (row1 + 31) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * kSellWarps;
+  const int64_t first = t0 + (int64_t)blockIdx.x * kSellWarps + warp;
+  if (first >= t1) return;
+
+  // ---- producer (lane 0): streams the items (tile, j-chunk) of this warp's tiles
+  int64_t p_tile = first, p_j = 0, p_len = 0;
+  auto p_issue = [&](int s) {
+    const int64_t base = toff[p_tile];
+    const int nj = (int)min((int64_t)kSellCJ, p_len - p_j);
+    const uint32_t vb = (uint32_t)nj * 256u, cb = (uint32_t)nj * 128u;
+    mbar_expect_tx(&full[s], vb + cb);  // 0 bytes (empty tile) completes the phase at once
+    if (nj > 0) {
+      tma_bulk_g2s(const_cast<double*>(stv(s)), sval + base + p_j * 32, vb, &full[s]);
+      tma_bulk_g2s(const_cast<int32_t*>(stc(s)), scol + base + p_j * 32, cb, &full[s]);
+    }
+    p_j += kSellCJ;
+    if (p_j >= p_len) {  // every tile has >= 1 item, so empty rows still write 0
+      p_tile += nwarps;
+      p_j = 0;
+      if (p_tile < t1) p_len = (toff[p_tile + 1] - toff[p_tile]) / 32;
+    }
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kSellS; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    p_len = (toff[p_tile + 1] - toff[p_tile]) / 32;
+#pragma unroll
+    for (int s = 0; s < kSellS; ++s)
+      if (p_tile < t1) p_issue(s);
+  }
+  __syncwarp();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t tile = first; tile < t1; tile += nwarps) {
+    const int64_t r = tile * 32 + lane;
+    const bool mine = r >= row0 && r < row1;
+    const int len = mine ? (int)((int64_t)row_ptr[r + 1] - (int64_t)row_ptr[r]) : 0;
+    const int64_t pm = (mine && perm) ? (int64_t)perm[r] : 0;
+    const int64_t tlen = (toff[tile + 1] - toff[tile]) / 32;
+    double acc = 0.0;
+    int64_t j0 = 0;
+    do {
+      mbar_wait(&full[stage], phase);
+      const double* sv = stv(stage);
+      const int32_t* sc = stc(stage);
+      const int cnt = (int)max((int64_t)0, min((int64_t)kSellCJ, (int64_t)len - j0));
+      for (int jj = 0; jj < cnt; jj += kSellB) {
+        int c[kSellB];
+        double g[kSellB];
+#pragma unroll
+        for (int u = 0; u < kSellB; ++u) c[u] = jj + u < cnt ? sc[(jj + u) * 32 + lane] : 0;
+#pragma unroll
+        for (int u = 0; u < kSellB; ++u)
+          if (jj + u < cnt) g[u] = ld_keep(x + c[u], keep);
+#pragma unroll
+        for (int u = 0; u < kSellB; ++u)
+          if (jj + u < cnt) acc = __dadd_rn(acc, __dmul_rn(sv[(jj + u) * 32 + lane], g[u]));
+      }
+      __syncwarp();
+      if (lane == 0 && p_tile < t1) {  // stage consumed: refill it S items ahead
+        fence_proxy_async_smem();
+        p_issue(stage);
+      }
+      if (++stage == kSellS) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      j0 += kSellCJ;
+    } while (j0 < tlen);
+    if (mine) {
+      if (perm) y[pm] = acc;
+      else y[r - row0] = acc;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace hb
+
+extern "C" int hb_spmv_sell_build(const int32_t* row_ptr, const int32_t* col_idx, const double* values, int64_t rows,
+                                  int64_t* tile_off, int32_t* sell_col, double* sell_val, int64_t* total_out,
+                                  int flags, void* stream) {
+  using namespace hb;
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_spmv_sell_build works on device arrays");
+  HB_CHECK_ARG(rows >= 1 && row_ptr && tile_off && total_out, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  const int64_t ntiles = ceil_div(rows, 32);
+  if (sell_col == nullptr) {  // sizing: tile_off (ntiles+1, device) and the total element count
+    int64_t g = ceil_div(ntiles, 256);
+    if (g > (int64_t)di.sms * 16) g = (int64_t)di.sms * 16;
+    sell_size_kernel<<<(int)g, 256, 0, s>>>(row_ptr, rows, tile_off);
+    sell_scan_kernel<<<1, 1024, 0, s>>>(tile_off, ntiles);
+    HB_TRY(check_launch());
+    HB_CUDA_TRY(cudaMemcpyAsync(total_out, tile_off + ntiles, 8, cudaMemcpyDeviceToHost, s));
+    HB_CUDA_TRY(cudaStreamSynchronize(s));
+    return HB_OK;
+  }
+  HB_CHECK_ARG(col_idx && values && sell_val, "NULL pointer");
+  int64_t g = ceil_div(ntiles, 8);
+  if (g > (int64_t)di.sms * 16) g = (int64_t)di.sms * 16;
+  sell_fill_kernel<<<(int)g, 256, 0, s>>>(row_ptr, col_idx, values, rows, tile_off, sell_col, sell_val);
+  return finish(flags, s);
+}
+
+extern "C" int hb_spmv_sell(const int32_t* row_ptr, const int64_t* tile_off, const int32_t* sell_col,
+                            const double* sell_val, int64_t row0, int64_t row1, const double* x, const void* perm,
+                            int perm_code, double* y, int flags, void* stream) {
+  using namespace hb;
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_spmv_sell works on device arrays");
+  HB_CHECK_ARG(row0 >= 0 && row1 >= row0, "bad row range");
+  HB_CHECK_ARG(perm == nullptr || idx_size_ok(perm_code), "perm must be int32 or int64");
+  if (row1 == row0) return HB_OK;
+  cudaStream_t s = as_stream(stream);
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  const int64_t ntiles = (row1 + 31) / 32 - row0 / 32;
+  int64_t grid = (int64_t)di.sms * kSellMinB;
+  if (grid > ceil_div(ntiles, kSellWarps)) grid = ceil_div(ntiles, kSellWarps);
+  int rc;
+  if (perm == nullptr || perm_code == HB_I32) {
+    auto k = spmv_sell_kernel<int32_t>;
+    HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellBytes));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     carveout_pct(kSellMinB * (kSellBytes + 256 + 1024))));
+    k<<<(unsigned)grid, 32 * kSellWarps, kSellBytes, s>>>(row_ptr, tile_off, sell_col, sell_val, x, row0, row1,
+                                                          reinterpret_cast<const int32_t*>(perm), y);
+    rc = check_launch();
+  } else {
+    auto k = spmv_sell_kernel<int64_t>;
+    HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellBytes));
+    HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     carveout_pct(kSellMinB * (kSellBytes + 256 + 1024))));
+    k<<<(unsigned)grid, 32 * kSellWarps, kSellBytes, s>>>(row_ptr, tile_off, sell_col, sell_val, x, row0, row1,
+                                                          reinterpret_cast<const int64_t*>(perm), y);
+    rc = check_launch();
+  }
+  if (rc != HB_OK) return rc;
+  return finish(flags, s);
+}

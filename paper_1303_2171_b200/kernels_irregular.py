@@ -309,11 +309,41 @@ def _host_range_matvec(m: CsrMatrix, x: np.ndarray, row0: int, row1: int, worker
     return y
 
 
+def sell_layout(m: CsrMatrix):
+    """The SELL-32 copy of a device int32 matrix (hb_spmv_sell_build), built
+    once and cached on the matrix (device matrices are not mutated in place):
+    (tile_off int64[ntiles+1], col int32[total], val float64[total])."""
+    import ctypes
+
+    import torch
+
+    cached = getattr(m, "_sell", None)
+    if cached is not None:
+        return cached
+    ntiles = (m.rows + 31) // 32
+    dev = m.row_ptr.device
+    toff = torch.empty(ntiles + 1, dtype=torch.int64, device=dev)
+    total = ctypes.c_int64(0)
+    st = current_stream_handle(m.row_ptr)
+    _lib.call("hb_spmv_sell_build", vp(m.row_ptr.data_ptr()), None, None, m.rows, vp(toff.data_ptr()), None, None,
+              ctypes.byref(total), _lib.HB_DEVICE_PTRS, st)
+    scol = torch.empty(total.value, dtype=torch.int32, device=dev)
+    sval = torch.empty(total.value, dtype=torch.float64, device=dev)
+    _lib.call("hb_spmv_sell_build", vp(m.row_ptr.data_ptr()), vp(m.col_idx.data_ptr()), vp(m.values.data_ptr()),
+              m.rows, vp(toff.data_ptr()), vp(scol.data_ptr()), vp(sval.data_ptr()), ctypes.byref(total),
+              _lib.HB_DEVICE_PTRS, st)
+    layout = (toff, scol, sval)
+    object.__setattr__(m, "_sell", layout)
+    return layout
+
+
 def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: Any = None,
              *, exact: bool = True, method: str | None = None, asynchronous: bool = False) -> Any:
     """DeviceB body (hb_spmv_csr).  Without `perm` returns/fills the y_perm
     slice of rows [row0, row1); with `perm` scatters y[perm[i]] in place.
-    `method`: "exact" (default; bit-exact sequential row sums), "warp"
+    `method`: "exact" (default; bit-exact sequential row sums — on a device
+    int32 matrix through its cached SELL-32 copy, `sell_layout`),
+    "exact_csr" (the same arithmetic straight from the CSR arrays), "warp"
     (warp-per-row tree sums) or "merge" (merge-path, load-balanced for any
     row-length distribution without preprocessing) — the last two within 1e-9
     relative.  `exact=False` is the older spelling of "warp"."""
@@ -321,7 +351,8 @@ def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: An
     if row1 > row0:
         require_gpu()
     method = method or ("exact" if exact else "warp")
-    modes = {"exact": _lib.HB_SPMV_SEQ, "warp": _lib.HB_SPMV_WARP, "merge": _lib.HB_SPMV_MERGE}
+    modes = {"exact": _lib.HB_SPMV_SEQ, "exact_csr": _lib.HB_SPMV_SEQ, "warp": _lib.HB_SPMV_WARP,
+             "merge": _lib.HB_SPMV_MERGE}
     if method not in modes:
         raise ValueError(f"unknown SpMV method {method!r}")
     mode = modes[method]
@@ -335,6 +366,13 @@ def gpu_spmv(m: CsrMatrix, x: Any, row0: int, row1: int, y: Any = None, perm: An
         if row1 == row0:
             return y
         flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0)
+        if method == "exact" and m.row_ptr.dtype == torch.int32 and m.col_idx.dtype == torch.int32:
+            toff, scol, sval = sell_layout(m)
+            _lib.call("hb_spmv_sell", vp(m.row_ptr.data_ptr()), vp(toff.data_ptr()), vp(scol.data_ptr()),
+                      vp(sval.data_ptr()), row0, row1, vp(x.data_ptr()),
+                      vp(perm.data_ptr() if perm is not None else 0), _index_code(perm) if perm is not None else 0,
+                      vp(y.data_ptr()), flags, current_stream_handle(x))
+            return y
         _lib.call(
             "hb_spmv_csr", vp(m.row_ptr.data_ptr()), _index_code(m.row_ptr), vp(m.col_idx.data_ptr()),
             _index_code(m.col_idx), vp(m.values.data_ptr()), row0, row1, m.cols, vp(x.data_ptr()),

@@ -128,25 +128,47 @@ def out_like(device: bool, shape: Any, dtype: Any, ref: Any = None) -> Any:
 
 PINNED_MIN_BYTES = 4 << 20
 PINNED_MAX_BYTES = 8 << 30
+PINNED_LIVE_CAP = 4 << 30  # pinned result bytes a caller may hold at once
+
+_pinned_live = [0]  # bytes of pinned results still referenced by callers
+_pinned_lock = __import__("threading").Lock()
+
+
+def _pinned_released(nbytes: int) -> None:
+    with _pinned_lock:
+        _pinned_live[0] -= nbytes
 
 
 def host_empty(shape: Any, dtype: Any = np.float64) -> np.ndarray:
     """An uninitialised host array for a result the GPU writes back.  Large
     results come from torch's caching pinned-host allocator (a numpy view
     that keeps its block alive; the block returns to the cache when the
-    array is dropped), so the D2H is one DMA straight into the result — no
-    pageable staging pass, no first-touch page faults on a fresh multi-GB
-    np.empty.  Small results, results above PINNED_MAX_BYTES and hosts
-    without CUDA get a plain np.empty."""
+    array is dropped), so the D2H is one DMA straight into the result.  A
+    caller that KEEPS its results would make every call pin fresh memory
+    (cudaHostAlloc: far slower than the copy it saves), so once the live
+    pinned results exceed PINNED_LIVE_CAP further results are plain
+    np.empty (the library copies into them through its pinned stages).
+    Small results, results above PINNED_MAX_BYTES and hosts without CUDA get
+    a plain np.empty too."""
+    import weakref
+
     dt = np.dtype(dtype)
     shape = (int(shape),) if np.ndim(shape) == 0 else tuple(int(d) for d in shape)
     nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
     if (torch is not None and PINNED_MIN_BYTES <= nbytes <= PINNED_MAX_BYTES and dt in _TORCH_TO_NP.values()
             and torch.cuda.is_available()):
-        try:
-            return torch.empty(shape, dtype=_np_to_torch(dt), pin_memory=True).numpy()
-        except RuntimeError:  # pinned memory exhausted: pageable result
-            pass
+        with _pinned_lock:
+            fits = _pinned_live[0] + nbytes <= PINNED_LIVE_CAP
+            if fits:
+                _pinned_live[0] += nbytes
+        if fits:
+            try:
+                arr = torch.empty(shape, dtype=_np_to_torch(dt), pin_memory=True).numpy()
+            except RuntimeError:  # pinned memory exhausted: pageable result
+                _pinned_released(nbytes)
+            else:
+                weakref.finalize(arr, _pinned_released, nbytes)
+                return arr
     return np.empty(shape, dtype=dt)
 
 

@@ -141,3 +141,24 @@ def test_calibrate_measured_on_a_host_only_workload():
     assert len(share.probe.refinement_steps) >= 3 + 2  # start, refinements, both ends
     seq = calibrate_measured(wl, p, max_refinements=2, concurrent=False)
     assert 0.0 <= seq.fraction_a <= 1.0
+
+
+def test_resolve_share_modes(platform13):
+    """resolve_share (reference workloads.py:73-79) over every ShareSpec mode,
+    and ShareSpec's validation (config.py:91-106)."""
+    from paper_1303_2171_b200.errors import ConfigError
+    from paper_1303_2171_b200.worksharing import ShareSpec, resolve_share
+
+    assert resolve_share(platform13, ShareSpec(), 100.0).fraction_a == pytest.approx(0.25)
+    assert resolve_share(platform13, ShareSpec("manual", 0.4), 100.0).fraction_a == 0.4
+    cal = resolve_share(platform13, ShareSpec("calibrated", refinements=6), 0.0)
+    assert cal.origin.value == "calibrated" and cal.fraction_a == pytest.approx(0.25)
+    assert cal.probe.sample_size == 1.0  # max(total_units, 1)
+    with pytest.raises(ConfigError):
+        ShareSpec("sometimes")
+    with pytest.raises(ConfigError):
+        ShareSpec("manual", 1.5)
+    with pytest.raises(ConfigError):
+        ShareSpec("calibrated", refinements=-1)
+    with pytest.raises(ValueError):
+        resolve_share(platform13, ShareSpec("measured", refinements=1), 10.0)

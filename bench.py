@@ -333,7 +333,7 @@ class SpmvBench(Bench):
     nnz-sorted by the device spmv_preprocess; one step = y = A x over all
     rows, original row order."""
 
-    name, unit, kernel = "spmv", "GFLOP/s", "spmv_lpr_kernel"
+    name, unit, kernel = "spmv", "GFLOP/s", "spmv_sell_kernel"
     CONFIG, LARGEST = 1_000_000, 1 << 24
     AVG_DENSITY_COLS = 16.000000000000004  # 1.6e-5 * 1e6: the config's nnz/row target
 
@@ -492,10 +492,33 @@ class BilatBench(Bench):
 
         self.lut = build_bilateral_lut(self.radius, max(self.radius / 2.0, 0.5), 40.0)
 
-    def rows_fn(self, a, b, out=None):
+    def rows_fn(self, a, b, out=None, arithmetic="fp64"):
         from paper_1303_2171_b200.kernels_regular import gpu_bilateral_rows
 
-        return gpu_bilateral_rows(self.img, self.lut, a, b, out=out, out_dtype=np.float32, asynchronous=True)
+        return gpu_bilateral_rows(self.img, self.lut, a, b, out=out, out_dtype=np.float32, asynchronous=True,
+                                  arithmetic=arithmetic)
+
+    def extra(self, args):
+        """The fp32-arithmetic mode (north_star: filter outputs within 1e-5
+        relative), device-resident, N=1: value + agreement with the fp64 kernel."""
+        import torch
+
+        if self.world > 1:
+            return {}
+        for _ in range(3):
+            self.rows_fn(0, self.height, out=self.out, arithmetic="fp32")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            self.rows_fn(0, self.height, out=self.out, arithmetic="fp32")
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.steps
+        ref = self.rows_fn(0, self.height)  # fp64 taps
+        torch.cuda.synchronize()
+        err = float(((self.out.double() - ref.double()).abs() / ref.double().abs().clamp_min(1e-30)).max())
+        return {"fp32": {"value": self.units_per_step() / (ms / 1e3) / 1e6, "ms_per_step": ms,
+                         "max_rel_err_vs_fp64": err, "parity": err <= 1e-5}}
 
     def config(self):
         return {"workload": f"{self.name}: {self.height}x{self.side} image, {2 * self.radius + 1}x{2 * self.radius + 1}"
@@ -605,10 +628,11 @@ class ConvBench(BilatBench):
 
         self.fk = FilterKernel.gaussian(self.radius)
 
-    def rows_fn(self, a, b, out=None):
+    def rows_fn(self, a, b, out=None, arithmetic="fp64"):
         from paper_1303_2171_b200.kernels_regular import gpu_convolve_rows
 
-        return gpu_convolve_rows(self.img, self.fk, a, b, out=out, out_dtype=np.float32, asynchronous=True)
+        return gpu_convolve_rows(self.img, self.fk, a, b, out=out, out_dtype=np.float32, asynchronous=True,
+                                 arithmetic=arithmetic)
 
     def flops_per_launch(self):
         return self.height * self.side * (2 * self.radius + 1) ** 2 * 2 // self.world
@@ -767,7 +791,7 @@ class LrBench(Bench):
     (gen_list(2^28, 42), generated on the device bit-identically), succ int32,
     ranks int64; N>1: the sharded sublist ranking (strong scaling)."""
 
-    name, unit, kernel = "lr", "Mnodes/s", "lr_walk_kernel"
+    name, unit, kernel = "lr", "Mnodes/s", "lr_walk_log_kernel"
     CONFIG, LARGEST = 1 << 28, 1 << 29
     always_strong = True
 
@@ -959,6 +983,7 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
         clk = clocks.summary(t0, t1)
     ms = reduce_over_ranks(ms, world, "max")
     ok = reduce_over_ranks(float(wl.verify()), world, "min") == 1.0
+    extra = wl.extra(args) if hasattr(wl, "extra") else {}
 
     # end to end through the public API (host buffers)
     wl.e2e_setup()
@@ -1019,6 +1044,7 @@ def measure(args, wl, rank, world, with_cpu: bool) -> dict:
                              "inputs": "pageable numpy arrays, every result kept (what a plain caller does)"}},
         "clocks": clk,
         "config": wl.config(),
+        **extra,
     }
     if with_cpu and rank == 0:
         fn, units, sample, cores, kind, _ = wl.cpu_sample()
@@ -1038,6 +1064,9 @@ def compact(res: dict) -> dict:
            "n": res["config"]["n_global"]}
     if "compute" in rl:
         out["fp64_frac"] = round(rl["compute"]["frac"], 3)
+    if "fp32" in res:
+        out["v_fp32"] = round(res["fp32"]["value"], 1)
+        out["ok"] = out["ok"] and bool(res["fp32"]["parity"])
     if "random_access" in rl:
         out["ra_frac"] = round(rl["random_access"]["frac"], 3)
     if "cpu_baseline" in res:

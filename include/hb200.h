@@ -160,7 +160,11 @@ int hb_gen_csr(int64_t rows, int64_t cols, int64_t avg, uint64_t seed_counts, ui
  * spatial[(2r+1)^2] row-major and range256[256] are the BilateralLut tables
  * (:447-458).  out is (row1-row0) x width, fp64 (out_code 64, bit-identical
  * to the reference) or fp32 (out_code 32, the fp64 result rounded).
+ * flags & HB_FP32_ARITH: taps in fp32 (fp32 tables, FMA), within 1e-5
+ * relative of the fp64 result (the tolerance north_star allows for filter
+ * outputs) at about twice the fp64 kernel's rate.
  * Host-pointer calls stage only the strip plus its clamped halo rows.     */
+#define HB_FP32_ARITH 16  /* filters: fp32 arithmetic (within 1e-5 relative of the fp64 result) */
 int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t radius,
                     const double* spatial, const double* range256, int32_t row0, int32_t row1,
                     void* out, int out_code, int flags, void* stream);
@@ -172,6 +176,8 @@ int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t r
  * (2r+1)^2 row-major weights.  Bit-identical to the reference for fp64 output
  * (out_code 64): taps in row-major order, zero weights skipped, rounded fp64
  * multiply then add, no FMA.  out_code 32 rounds that result to fp32.
+ * flags & HB_FP32_ARITH: fp32 taps with FMA, within 1e-5 relative of the
+ * fp64 result (north_star's filter tolerance).
  * Host-pointer calls stage only the strip plus its clamped halo rows.     */
 int hb_convolve(const void* img, int in_code, int32_t height, int32_t width, int32_t radius,
                 const double* weights, int32_t row0, int32_t row1, void* out, int out_code,

@@ -126,7 +126,11 @@ struct TmaTile {
 // its fp64 conversion) serves all NR rows; per pixel the taps stay in
 // row-major order, so the result is bit-identical.
 
-template <int R, typename OUT, int NR, int MINB, bool SYM = false>
+// ACC = float: the fp32-arithmetic mode (north_star: filter outputs within
+// 1e-5 relative): fp32 tables striped over 32 lanes (the same 128-byte table
+// rows), w = s·r, num = fma(w, nb, num), den += w — half the issue slots of
+// the fp64 tap and one shared wavefront per warp-tap instead of two.
+template <int R, typename OUT, int NR, int MINB, bool SYM = false, typename ACC = double>
 __global__ void __launch_bounds__(kThreads, MINB)
     bilateral_tma_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ img, int H, int W,
                          int row0, int row1, const double* __restrict__ spatial, const double* __restrict__ range,
@@ -140,11 +144,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // rows, entry 255+e = range[|e|]), so a tap indexes it with nb - c directly
   // — no IABS — at twice the shared memory
   constexpr int NE = SYM ? 511 : 256;
+  constexpr int ST = 128 / (int)sizeof(ACC);  // table stripes: one 128-byte row per intensity
   uint8_t* tile = smem;                                                     // [TH][TWB], 128-B aligned
-  double* rng = reinterpret_cast<double*>(smem + ((TH * TWB + 127) / 128) * 128);  // [NE][16]
-  double* sp = rng + NE * 16;                                               // [S*S]
+  ACC* rng = reinterpret_cast<ACC*>(smem + ((TH * TWB + 127) / 128) * 128);  // [NE][ST]
+  ACC* sp = rng + NE * ST;                                                  // [S*S]
   const int tid = threadIdx.x;
-  const int lane = tid & 15;
+  const int lane = tid & (ST - 1);
   const int y0 = row0 + blockIdx.y * T::TILE_H;
   const int x0 = blockIdx.x * kTileW;
   const bool interior = x0 - T::PADX >= 0 && x0 - T::PADX + TWB <= W && y0 - R >= 0 && y0 - R + TH <= H;
@@ -158,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
         ::"r"(d), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(x0 - T::PADX), "r"(y0 - R), "r"(b) : "memory");
   }
-  for (int i = tid; i < NE * 16; i += kThreads) rng[i] = range[SYM ? abs((i >> 4) - 255) : (i >> 4)];
-  for (int i = tid; i < S * S; i += kThreads) sp[i] = spatial[i];
+  for (int i = tid; i < NE * ST; i += kThreads) rng[i] = (ACC)range[SYM ? abs(i / ST - 255) : i / ST];
+  for (int i = tid; i < S * S; i += kThreads) sp[i] = (ACC)spatial[i];
   if (!interior) {
     for (int i = tid; i < TH * TW; i += kThreads) {
       const int ty = i / TW, tx = i - ty * TW;
@@ -176,15 +181,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const int gy = y0 + py;
   if (gy >= row1) return;
   int c[NR][kPx];
-  double num[NR][kPx], den[NR][kPx];
+  ACC num[NR][kPx], den[NR][kPx];
 #pragma unroll
   for (int k = 0; k < NR; ++k)
 #pragma unroll
     for (int j = 0; j < kPx; ++j) {
       c[k][j] = tile[(py + k + R) * TWB + px + j + R + OFF];
-      num[k][j] = den[k][j] = 0.0;
+      num[k][j] = den[k][j] = (ACC)0;
     }
-  const double* lane_rng = rng + lane + (SYM ? 255 * 16 : 0);
+  const ACC* lane_rng = rng + lane + (SYM ? 255 * ST : 0);
   // SYM: per-pixel shared-memory byte address of range[nb - c] is
   // cbase[j] + nb*128 (the table row of difference 0, minus c rows), so a tap
   // costs one 32-bit add + one LDS instead of subtract + multiply-add
@@ -199,13 +204,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll 1
   for (int iy = 0; iy < S + NR - 1; ++iy) {
     int nb[kPx + 2 * R];
-    double nbd[kPx + 2 * R];
+    ACC nbd[kPx + 2 * R];
     const uint8_t* trow = tile + (py + iy) * TWB + px + OFF;
 #pragma unroll
     for (int q = 0; q < kPx + 2 * R; ++q) nb[q] = trow[q];
 #pragma unroll
     for (int q = 0; q < kPx + 2 * R; ++q) {
-      nbd[q] = (double)nb[q];
+      nbd[q] = (ACC)nb[q];
       if (SYM) nb[q] *= 128;  // byte offset of the intensity's table row
     }
 #pragma unroll
@@ -214,18 +219,23 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (dy < 0 || dy >= S) continue;
 #pragma unroll
       for (int dx = 0; dx < S; ++dx) {
-        const double s = sp[dy * S + dx];
+        const ACC s = sp[dy * S + dx];
 #pragma unroll
         for (int j = 0; j < kPx; ++j) {
-          double r;
-          if (SYM) {
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(cbase[k][j] + (uint32_t)nb[j + dx]));
+          ACC r;
+          if constexpr (sizeof(ACC) == 8) {
+            if (SYM) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(cbase[k][j] + (uint32_t)nb[j + dx]));
+            else r = lane_rng[abs(nb[j + dx] - c[k][j]) * ST];
+            const double w = __dmul_rn(s, r);  // the reference's op order, no FMA (bit-exact)
+            num[k][j] = __dadd_rn(num[k][j], __dmul_rn(w, nbd[j + dx]));
+            den[k][j] = __dadd_rn(den[k][j], w);
           } else {
-            r = lane_rng[abs(nb[j + dx] - c[k][j]) * 16];
+            if (SYM) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(cbase[k][j] + (uint32_t)nb[j + dx]));
+            else r = lane_rng[abs(nb[j + dx] - c[k][j]) * ST];
+            const float w = s * r;
+            num[k][j] = fmaf(w, nbd[j + dx], num[k][j]);
+            den[k][j] = den[k][j] + w;
           }
-          const double w = __dmul_rn(s, r);
-          num[k][j] = __dadd_rn(num[k][j], __dmul_rn(w, nbd[j + dx]));
-          den[k][j] = __dadd_rn(den[k][j], w);
         }
       }
     }
@@ -236,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     OUT* o = out + (int64_t)(gy + k - row0) * W + x0 + px;
 #pragma unroll
     for (int j = 0; j < kPx; ++j)
-      if (x0 + px + j < W) o[j] = (OUT)__ddiv_rn(num[k][j], den[k][j]);
+      if (x0 + px + j < W) {
+        if constexpr (sizeof(ACC) == 8) o[j] = (OUT)__ddiv_rn(num[k][j], den[k][j]);
+        else o[j] = (OUT)__fdiv_rn(num[k][j], den[k][j]);
+      }
   }
 }
 
@@ -290,16 +303,16 @@ __global__ void bilateral_generic_kernel(const uint8_t* __restrict__ img, int H,
 
 template <int R, typename OUT>
 int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const double* sp,
-                const double* rg, OUT* out, cudaStream_t s) {
+                const double* rg, OUT* out, bool fp32, cudaStream_t s) {
   constexpr int S = 2 * R + 1;
   // TMA-staged halo tiles, one row per thread, signed 511-entry range table
-  // striped over 16 lanes, 3 CTAs/SM (measured best)
+  // striped over 16 lanes (fp64) / 32 lanes (fp32), 3 CTAs/SM (measured best)
   {
     using T = TmaTile<R, 1>;
-    auto kern = bilateral_tma_kernel<R, OUT, 1, 3, true>;
+    auto kern = fp32 ? bilateral_tma_kernel<R, OUT, 1, 3, true, float> : bilateral_tma_kernel<R, OUT, 1, 3, true, double>;
     CUtensorMap map;
     if (make_image_tmap(&map, img, H, W, T::TWB, T::TH)) {
-      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + 511 * 16 * 8 + S * S * 8;
+      const size_t smem = (size_t)(T::TH * T::TWB + 127) / 128 * 128 + 511 * 128 + S * S * (fp32 ? 4 : 8);
       HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, T::TILE_H));
       kern<<<grid, kThreads, smem, s>>>(map, img, H, W, row0, row1, sp, rg, out);
@@ -318,17 +331,17 @@ int launch_tile(const uint8_t* img, int H, int W, int row0, int row1, const doub
 
 template <typename OUT>
 int launch_bilateral(const uint8_t* img, int H, int W, int row0, int row1, int R, const double* sp,
-                     const double* rg, OUT* out, cudaStream_t s) {
+                     const double* rg, OUT* out, bool fp32, cudaStream_t s) {
   switch (R) {
-    case 0: return launch_tile<0, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 1: return launch_tile<1, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 2: return launch_tile<2, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 3: return launch_tile<3, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 4: return launch_tile<4, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 5: return launch_tile<5, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 6: return launch_tile<6, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 7: return launch_tile<7, OUT>(img, H, W, row0, row1, sp, rg, out, s);
-    case 8: return launch_tile<8, OUT>(img, H, W, row0, row1, sp, rg, out, s);
+    case 0: return launch_tile<0, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 1: return launch_tile<1, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 2: return launch_tile<2, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 3: return launch_tile<3, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 4: return launch_tile<4, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 5: return launch_tile<5, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 6: return launch_tile<6, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 7: return launch_tile<7, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
+    case 8: return launch_tile<8, OUT>(img, H, W, row0, row1, sp, rg, out, fp32, s);
     default: {
       DeviceInfo di;
       HB_TRY(device_info(&di));
@@ -358,6 +371,7 @@ extern "C" int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width
   const bool dev = flags & HB_DEVICE_PTRS;
   HB_CHECK_ARG(dev || !(flags & HB_ASYNC), "HB_ASYNC requires device pointers");
   cudaStream_t s = as_stream(stream);
+  const bool fp32 = flags & HB_FP32_ARITH;
   const int S = 2 * radius + 1;
   // host calls: stage only the strip and its clamped halo rows
   int in0 = 0, in1 = height;
@@ -377,8 +391,8 @@ extern "C" int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width
   auto launch = [&](int a, int b) -> int {  // absolute rows [a, b)
     char* o = d_out.as<char>() + (size_t)(a - row0) * width * es;
     return out_code == 64
-               ? launch_bilateral<double>(d_img.as<uint8_t>(), h, width, a - in0, b - in0, radius, d_sp.as<double>(), d_rg.as<double>(), reinterpret_cast<double*>(o), s)
-               : launch_bilateral<float>(d_img.as<uint8_t>(), h, width, a - in0, b - in0, radius, d_sp.as<double>(), d_rg.as<double>(), reinterpret_cast<float*>(o), s);
+               ? launch_bilateral<double>(d_img.as<uint8_t>(), h, width, a - in0, b - in0, radius, d_sp.as<double>(), d_rg.as<double>(), reinterpret_cast<double*>(o), fp32, s)
+               : launch_bilateral<float>(d_img.as<uint8_t>(), h, width, a - in0, b - in0, radius, d_sp.as<double>(), d_rg.as<double>(), reinterpret_cast<float*>(o), fp32, s);
   };
   if (dev) {
     d_img.ptr = const_cast<uint8_t*>(img);

@@ -19,6 +19,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -48,26 +49,31 @@ __device__ __forceinline__ double to_f64(IN v) { return (double)v; }
 // ≡ 2·odd mod 16 doubles) — conflict-free, where the row-major lane order
 // put 4 lanes on each slot (ncu: 61 % of the shared wavefronts were
 // conflicts).  Same pixels per thread, same tap order.
-template <int R, typename IN, typename OUT, bool DENSE, int MINB, int NR>
+//
+// ACC = float: the fp32-arithmetic mode (within 1e-5 relative of the fp64
+// result, north_star's filter tolerance): fp32 tile and weights, one FMA per
+// tap, 8-byte (float2) segment loads — the same lane mapping stays
+// conflict-free (row stride 3·78 ≡ 10 mod 32 banks).
+template <int R, typename IN, typename OUT, bool DENSE, int MINB, int NR, typename ACC = double>
 __global__ void __launch_bounds__(kThreads, MINB)
     conv_rows_kernel(const IN* __restrict__ img, int H, int W, int row0, int row1,
                      const double* __restrict__ weights, OUT* __restrict__ out) {
   constexpr int S = 2 * R + 1;
-  constexpr int SWP = (S * S + 1) & ~1;  // weights padded so the tile is 16-B aligned
+  constexpr int SWP = (S * S + 3) & ~3;  // weights padded so the tile is 16-B aligned
   constexpr int TILE_H = kTileH * NR;
   constexpr int TH = TILE_H + 2 * R, TW = kTileW + 2 * R;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* sw = reinterpret_cast<double*>(smem);  // [S*S]
-  double* tile = sw + SWP;                       // [TH][TW]
+  ACC* sw = reinterpret_cast<ACC*>(smem);  // [S*S]
+  ACC* tile = sw + SWP;                    // [TH][TW]
   const int tid = threadIdx.x;
   const int y0 = row0 + blockIdx.y * TILE_H;
   const int x0 = blockIdx.x * kTileW;
-  for (int i = tid; i < S * S; i += kThreads) sw[i] = weights[i];
+  for (int i = tid; i < S * S; i += kThreads) sw[i] = (ACC)weights[i];
   for (int i = tid; i < TH * TW; i += kThreads) {
     const int ty = i / TW, tx = i - ty * TW;
     const int gy = min(max(y0 - R + ty, 0), H - 1);
     const int gx = min(max(x0 - R + tx, 0), W - 1);
-    tile[i] = to_f64(img[(int64_t)gy * W + gx]);
+    tile[i] = (ACC)to_f64(img[(int64_t)gy * W + gx]);
   }
   __syncthreads();
   static_assert(kTileW / kPx == 8 && kThreads % 32 == 0, "lane mapping assumes 8 pixel groups per row");
@@ -77,19 +83,20 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const int px = (lane >> 2) * kPx;
   const int gy = y0 + py;
   if (gy >= row1) return;
-  double acc[NR][kPx];
+  ACC acc[NR][kPx];
 #pragma unroll
   for (int k = 0; k < NR; ++k)
 #pragma unroll
-    for (int j = 0; j < kPx; ++j) acc[k][j] = 0.0;
+    for (int j = 0; j < kPx; ++j) acc[k][j] = (ACC)0;
 #pragma unroll 1
   for (int iy = 0; iy < S + NR - 1; ++iy) {  // input rows py .. py+S+NR-2 of the tile
-    double seg[kPx + 2 * R];
-    const double* trow = tile + (py + iy) * TW + px;
-    static_assert(TW % 2 == 0 && (kPx + 2 * R) % 2 == 0, "16-byte segment loads");
+    ACC seg[kPx + 2 * R];
+    const ACC* trow = tile + (py + iy) * TW + px;
+    static_assert(TW % 2 == 0 && (kPx + 2 * R) % 2 == 0, "two-element segment loads");
+    using V2 = typename std::conditional<sizeof(ACC) == 8, double2, float2>::type;
 #pragma unroll
     for (int q = 0; q < (kPx + 2 * R) / 2; ++q) {
-      const double2 v = reinterpret_cast<const double2*>(trow)[q];
+      const V2 v = reinterpret_cast<const V2*>(trow)[q];
       seg[2 * q] = v.x;
       seg[2 * q + 1] = v.y;
     }
@@ -99,10 +106,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (dy >= 0 && dy < S) {
 #pragma unroll
         for (int dx = 0; dx < S; ++dx) {
-          const double w = sw[dy * S + dx];
-          if (DENSE || w != 0.0) {
+          const ACC w = sw[dy * S + dx];
+          if (DENSE || w != (ACC)0) {
 #pragma unroll
-            for (int j = 0; j < kPx; ++j) acc[k][j] = __dadd_rn(acc[k][j], __dmul_rn(w, seg[j + dx]));
+            for (int j = 0; j < kPx; ++j) {
+              if constexpr (sizeof(ACC) == 8) acc[k][j] = __dadd_rn(acc[k][j], __dmul_rn(w, seg[j + dx]));  // bit-exact
+              else acc[k][j] = fmaf(w, seg[j + dx], acc[k][j]);
+            }
           }
         }
       }
@@ -144,9 +154,10 @@ __global__ void conv_generic_kernel(const IN* __restrict__ img, int H, int W, in
 // r=7: 38 Gpix/s; 2 rows 0.68, 1 row 0.61 of the fp64 peak)
 template <int R, typename IN, typename OUT>
 int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w, bool dense, OUT* out,
-                cudaStream_t s) {
+                bool fp32, cudaStream_t s) {
   constexpr int S = 2 * R + 1, NR = 3;
-  const size_t smem = (size_t)((S * S + 1) & ~1) * 8 + (size_t)(kTileH * NR + 2 * R) * (kTileW + 2 * R) * 8;
+  const size_t es = fp32 ? 4 : 8;
+  const size_t smem = (size_t)((S * S + 3) & ~3) * es + (size_t)(kTileH * NR + 2 * R) * (kTileW + 2 * R) * es;
   dim3 grid((unsigned)ceil_div(W, kTileW), (unsigned)ceil_div(row1 - row0, kTileH * NR));
   auto launch = [&](auto kern) -> int {
     HB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -154,22 +165,25 @@ int launch_tile(const IN* img, int H, int W, int row0, int row1, const double* w
     return check_launch();
   };
   // all-non-zero weights: the branch-free variant; otherwise zero taps are skipped like the reference
+  if (fp32)
+    return dense ? launch(conv_rows_kernel<R, IN, OUT, true, 2, NR, float>)
+                 : launch(conv_rows_kernel<R, IN, OUT, false, 2, NR, float>);
   return dense ? launch(conv_rows_kernel<R, IN, OUT, true, 2, NR>) : launch(conv_rows_kernel<R, IN, OUT, false, 2, NR>);
 }
 
 template <typename IN, typename OUT>
 int launch_conv(const IN* img, int H, int W, int row0, int row1, int R, const double* w, bool dense, OUT* out,
-                cudaStream_t s) {
+                bool fp32, cudaStream_t s) {
   switch (R) {
-    case 0: return launch_tile<0, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 1: return launch_tile<1, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 2: return launch_tile<2, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 3: return launch_tile<3, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 4: return launch_tile<4, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 5: return launch_tile<5, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 6: return launch_tile<6, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 7: return launch_tile<7, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
-    case 8: return launch_tile<8, IN, OUT>(img, H, W, row0, row1, w, dense, out, s);
+    case 0: return launch_tile<0, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 1: return launch_tile<1, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 2: return launch_tile<2, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 3: return launch_tile<3, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 4: return launch_tile<4, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 5: return launch_tile<5, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 6: return launch_tile<6, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 7: return launch_tile<7, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
+    case 8: return launch_tile<8, IN, OUT>(img, H, W, row0, row1, w, dense, out, fp32, s);
     default: {
       DeviceInfo di;
       HB_TRY(device_info(&di));
@@ -183,10 +197,10 @@ int launch_conv(const IN* img, int H, int W, int row0, int row1, int R, const do
 
 template <typename IN>
 int dispatch_out(const void* img, int H, int W, int row0, int row1, int R, const double* w, bool dense,
-                 void* out, int out_code, cudaStream_t s) {
+                 void* out, int out_code, bool fp32, cudaStream_t s) {
   auto in = reinterpret_cast<const IN*>(img);
-  return out_code == 64 ? launch_conv<IN, double>(in, H, W, row0, row1, R, w, dense, reinterpret_cast<double*>(out), s)
-                        : launch_conv<IN, float>(in, H, W, row0, row1, R, w, dense, reinterpret_cast<float*>(out), s);
+  return out_code == 64 ? launch_conv<IN, double>(in, H, W, row0, row1, R, w, dense, reinterpret_cast<double*>(out), fp32, s)
+                        : launch_conv<IN, float>(in, H, W, row0, row1, R, w, dense, reinterpret_cast<float*>(out), fp32, s);
 }
 
 }  // namespace
@@ -207,6 +221,7 @@ extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t
   const bool dev = flags & HB_DEVICE_PTRS;
   HB_CHECK_ARG(dev || !(flags & HB_ASYNC), "HB_ASYNC requires device pointers");
   cudaStream_t s = as_stream(stream);
+  const bool fp32 = flags & HB_FP32_ARITH;
   const int S = 2 * radius + 1;
   const size_t es_in = in_code == HB_U8 ? 1 : 8;
   // host calls stage only the strip and its clamped halo rows
@@ -237,8 +252,8 @@ extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t
   auto launch = [&](int a, int b) -> int {  // absolute rows [a, b)
     void* o = d_out.as<char>() + (size_t)(a - row0) * width * es_out;
     return in_code == HB_U8
-               ? dispatch_out<uint8_t>(d_img.ptr, h, width, a - in0, b - in0, radius, d_w.as<double>(), dense, o, out_code, s)
-               : dispatch_out<double>(d_img.ptr, h, width, a - in0, b - in0, radius, d_w.as<double>(), dense, o, out_code, s);
+               ? dispatch_out<uint8_t>(d_img.ptr, h, width, a - in0, b - in0, radius, d_w.as<double>(), dense, o, out_code, fp32, s)
+               : dispatch_out<double>(d_img.ptr, h, width, a - in0, b - in0, radius, d_w.as<double>(), dense, o, out_code, fp32, s);
   };
   if (dev) {
     d_img.ptr = const_cast<void*>(img);

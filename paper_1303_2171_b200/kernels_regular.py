@@ -524,14 +524,19 @@ def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, worke
 
 
 def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, out: Any = None,
-                      *, out_dtype: Any = np.float64, asynchronous: bool = False) -> Any:
+                      *, out_dtype: Any = np.float64, asynchronous: bool = False,
+                      arithmetic: str = "fp64") -> Any:
     """DeviceB body (hb_convolve): rows [row0, row1) on the GPU, bit-identical
     to `convolve_rows` for fp64 output.  uint8 and float64 pixels go to the
     kernel as they are; other dtypes are widened to float64 first (exactly
     what `astype(np.float64)` does in the reference).  Host pixels → numpy
-    result; CUDA pixels → result tensor."""
+    result; CUDA pixels → result tensor.  arithmetic="fp32": fp32 taps with
+    FMA, within 1e-5 relative of the fp64 result."""
     _lib.load()
     code = 64 if np.dtype(out_dtype) == np.float64 else 32
+    if arithmetic not in ("fp64", "fp32"):
+        raise ValueError(f"arithmetic must be 'fp64' or 'fp32', got {arithmetic!r}")
+    math_flag = _lib.HB_FP32_ARITH if arithmetic == "fp32" else 0
     height, width = int(pixels.shape[0]), int(pixels.shape[1])
     if not 0 <= row0 <= row1 <= height:
         raise ValueError("bad row range")
@@ -551,7 +556,7 @@ def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, o
             return out
         wt = torch.from_numpy(w).to(pixels.device)
         in_code = _lib.DTYPE_CODES["u1" if pixels.dtype == torch.uint8 else "f8"]
-        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0)
+        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0) | math_flag
         _lib.call("hb_convolve", vp(pixels.data_ptr()), in_code, height, width, kernel.radius, vp(wt.data_ptr()),
                   row0, row1, vp(out.data_ptr()), code, flags, current_stream_handle(pixels))
         return out
@@ -564,7 +569,7 @@ def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, o
     if row1 == row0:
         return out
     _lib.call("hb_convolve", vp(img.ptr), img.code, height, width, kernel.radius, vp(w.ctypes.data),
-              row0, row1, vp(out.ctypes.data), code, 0, current_stream_handle())
+              row0, row1, vp(out.ctypes.data), code, math_flag, current_stream_handle())
     return out
 
 
@@ -577,9 +582,10 @@ class ConvolutionWorkload(_StripOutput):
     name = "conv"
     unit = "neighbor accumulations"
 
-    def __init__(self, image: Image, kernel: FilterKernel):
+    def __init__(self, image: Image, kernel: FilterKernel, arithmetic: str = "fp64"):
         self.image = image
         self.kernel = kernel
+        self.arithmetic = arithmetic  # "fp32": the GPU share's taps in fp32 (within 1e-5 relative)
         self._per_row = image.width * (2 * kernel.radius + 1) ** 2
 
     def partition(self, fraction_a: float):
@@ -593,18 +599,19 @@ class ConvolutionWorkload(_StripOutput):
     def run_part(self, device: Device, part) -> np.ndarray:
         strip = self._strip(part)
         if device.id is DeviceId.B:
+            ar = self.arithmetic
             if strip is not None:
-                return gpu_convolve_rows(self.image.pixels, self.kernel, part[0], part[1], out=strip)
+                return gpu_convolve_rows(self.image.pixels, self.kernel, part[0], part[1], out=strip, arithmetic=ar)
             return sharding.run_sharded_rows(
-                part[0], part[1], lambda a, b: gpu_convolve_rows(self.image.pixels, self.kernel, a, b)
+                part[0], part[1], lambda a, b: gpu_convolve_rows(self.image.pixels, self.kernel, a, b, arithmetic=ar)
             )
         return convolve_rows(self.image.pixels, self.kernel, part[0], part[1], device.worker_count, out=strip)
 
 
 def hybrid_convolve(image: Image, kernel: FilterKernel, platform: Platform,
-                    share: WorkShare | None = None) -> Image:
-    """kernels_regular.py:408-414."""
-    workload = ConvolutionWorkload(image, kernel)
+                    share: WorkShare | None = None, *, arithmetic: str = "fp64") -> Image:
+    """kernels_regular.py:408-414 (+ `arithmetic`, this package's fp32 mode)."""
+    workload = ConvolutionWorkload(image, kernel, arithmetic)
     result, _ = run_workshared(platform, workload, share or formula_share(platform), baselines=False)
     return result
 
@@ -673,12 +680,18 @@ def bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, workers
 
 
 def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out: Any = None,
-                       *, out_dtype: Any = np.float64, asynchronous: bool = False) -> Any:
+                       *, out_dtype: Any = np.float64, asynchronous: bool = False,
+                       arithmetic: str = "fp64") -> Any:
     """DeviceB body (hb_bilateral_u8): rows [row0, row1) on the GPU, bit-identical
     to `bilateral_rows` for fp64 output.  Host pixels → numpy result; CUDA
-    pixels (uint8 tensor) → result tensor (the LUT tables are staged per call)."""
+    pixels (uint8 tensor) → result tensor (the LUT tables are staged per call).
+    arithmetic="fp32": taps in fp32 with FMA — within 1e-5 relative of the
+    fp64 result (north_star's filter tolerance), about twice as fast."""
     _lib.load()
     code = 64 if np.dtype(out_dtype) == np.float64 else 32
+    if arithmetic not in ("fp64", "fp32"):
+        raise ValueError(f"arithmetic must be 'fp64' or 'fp32', got {arithmetic!r}")
+    math_flag = _lib.HB_FP32_ARITH if arithmetic == "fp32" else 0
     height, width = int(pixels.shape[0]), int(pixels.shape[1])
     if not 0 <= row0 <= row1 <= height:
         raise ValueError("bad row range")
@@ -697,7 +710,7 @@ def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out
             return out
         sp = torch.from_numpy(np.ascontiguousarray(lut.spatial_weights)).to(pixels.device)
         rg = torch.from_numpy(np.ascontiguousarray(lut.range_weights)).to(pixels.device)
-        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0)
+        flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0) | math_flag
         _lib.call("hb_bilateral_u8", vp(pixels.data_ptr()), height, width, lut.radius, vp(sp.data_ptr()),
                   vp(rg.data_ptr()), row0, row1, vp(out.data_ptr()), code, flags, current_stream_handle(pixels))
         return out
@@ -709,7 +722,7 @@ def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out
     sp = np.ascontiguousarray(lut.spatial_weights, dtype=np.float64)
     rg = np.ascontiguousarray(lut.range_weights, dtype=np.float64)
     _lib.call("hb_bilateral_u8", vp(img.ptr), height, width, lut.radius, vp(sp.ctypes.data),
-              vp(rg.ctypes.data), row0, row1, vp(out.ctypes.data), code, 0, current_stream_handle())
+              vp(rg.ctypes.data), row0, row1, vp(out.ctypes.data), code, math_flag, current_stream_handle())
     return out
 
 
@@ -721,9 +734,10 @@ class BilateralApplyWorkload(_StripOutput):
     name = "bilat"
     unit = "neighbor accumulations"
 
-    def __init__(self, image: Image, lut: BilateralLut):
+    def __init__(self, image: Image, lut: BilateralLut, arithmetic: str = "fp64"):
         self.image = image
         self.lut = lut
+        self.arithmetic = arithmetic  # "fp32": the GPU share's taps in fp32 (within 1e-5 relative)
         self._per_row = image.width * (2 * lut.radius + 1) ** 2
 
     def partition(self, fraction_a: float):
@@ -737,16 +751,18 @@ class BilateralApplyWorkload(_StripOutput):
     def run_part(self, device: Device, part) -> np.ndarray:
         strip = self._strip(part)
         if device.id is DeviceId.B:
+            ar = self.arithmetic
             if strip is not None:
-                return gpu_bilateral_rows(self.image.pixels, self.lut, part[0], part[1], out=strip)
+                return gpu_bilateral_rows(self.image.pixels, self.lut, part[0], part[1], out=strip, arithmetic=ar)
             return sharding.run_sharded_rows(
-                part[0], part[1], lambda a, b: gpu_bilateral_rows(self.image.pixels, self.lut, a, b)
+                part[0], part[1], lambda a, b: gpu_bilateral_rows(self.image.pixels, self.lut, a, b, arithmetic=ar)
             )
         return bilateral_rows(self.image.pixels, self.lut, part[0], part[1], device.worker_count, out=strip)
 
 
-def hybrid_bilateral(image: Image, lut: BilateralLut, platform: Platform, share: WorkShare | None = None) -> Image:
-    """kernels_regular.py:514-520."""
-    workload = BilateralApplyWorkload(image, lut)
+def hybrid_bilateral(image: Image, lut: BilateralLut, platform: Platform, share: WorkShare | None = None,
+                     *, arithmetic: str = "fp64") -> Image:
+    """kernels_regular.py:514-520 (+ `arithmetic`, this package's fp32 mode)."""
+    workload = BilateralApplyWorkload(image, lut, arithmetic)
     result, _ = run_workshared(platform, workload, share or formula_share(platform), baselines=False)
     return result

@@ -103,3 +103,31 @@ def test_tma_staged_tiles_bit_exact(radius):
     for r0, r1 in ((0, 400), (37, 301), (399, 400)):
         got = gpu_bilateral_rows(d, lut, r0, r1).cpu().numpy()
         assert np.array_equal(got, obil.rows(pix, sp, rg, radius, r0, r1)), (radius, r0, r1)
+
+
+@pytest.mark.parametrize("radius", [0, 1, 5, 7])
+def test_fp32_arithmetic_within_tolerance(radius):
+    """arithmetic="fp32" (fp32 taps, FMA): within 1e-5 relative of the fp64
+    reference arithmetic (north_star's filter tolerance), host and device
+    paths, fp32 and fp64 outputs, through the public API too."""
+    import torch
+
+    from oracle import bilateral as obil
+    from oracle import datasets as ods
+    from paper_1303_2171_b200.kernels_regular import Image, build_bilateral_lut, gpu_bilateral_rows, hybrid_bilateral
+    from paper_1303_2171_b200.platform import Platform
+
+    img = ods.image(301, radius + 3)
+    sig = max(radius / 2.0, 0.5)
+    lut = build_bilateral_lut(radius, sig, 40.0)
+    sp, rg = obil.lut(radius, sig, 40.0)
+    want = obil.rows(img, sp, rg, radius, 0, 301)
+    for out_dtype in (np.float32, np.float64):
+        got = gpu_bilateral_rows(torch.from_numpy(img).cuda(), lut, 0, 301, out_dtype=out_dtype, arithmetic="fp32")
+        assert np.allclose(got.cpu().numpy(), want, rtol=1e-5, atol=0), out_dtype
+        host = gpu_bilateral_rows(img, lut, 10, 200, out_dtype=out_dtype, arithmetic="fp32")
+        assert np.allclose(host, want[10:200], rtol=1e-5, atol=0)
+    res = hybrid_bilateral(Image(img), lut, Platform.build(1.0, 3.0), arithmetic="fp32").pixels
+    assert np.allclose(res, want, rtol=1e-5, atol=0)
+    with pytest.raises(ValueError):
+        gpu_bilateral_rows(img, lut, 0, 4, arithmetic="fp16")

@@ -139,3 +139,34 @@ def test_criterion_7_figure_reproduction():
     # and bit-exact with the reference arithmetic on a strip from each side
     for r0 in (600, 2000):
         assert np.array_equal(bits(out.pixels[r0 : r0 + 64]), bits(oconv.rows(img.pixels, k.weights, r0, r0 + 64)))
+
+
+@pytest.mark.parametrize("radius", [0, 2, 7, 8])
+def test_fp32_arithmetic_within_tolerance(radius):
+    """arithmetic="fp32": fp32 taps with FMA, within 1e-5 relative of the fp64
+    reference arithmetic (absolute floor: 1e-5 of the largest possible
+    |output|, for outputs near zero with signed weights); uint8 and float64
+    images, zero taps, the public API."""
+    import torch
+
+    from oracle import conv as oconv
+    from oracle import datasets as ods
+    from paper_1303_2171_b200.kernels_regular import FilterKernel, Image, gpu_convolve_rows, hybrid_convolve
+    from paper_1303_2171_b200.platform import Platform
+
+    rs = np.random.default_rng(radius)
+    img = ods.image(211, radius + 5)
+    for fk in (FilterKernel.gaussian(radius), FilterKernel(rs.standard_normal((2 * radius + 1,) * 2))):
+        w = fk.weights.copy()
+        if w.size > 1:
+            w.flat[::3] = 0.0  # zero taps
+        fk = FilterKernel(w)
+        for pix in (img, img.astype(np.float64) / 7.0):
+            want = oconv.rows(pix, fk.weights, 0, 211)
+            scale = np.abs(fk.weights).sum() * np.abs(pix).max()
+            got = gpu_convolve_rows(torch.from_numpy(pix).cuda(), fk, 0, 211, out_dtype=np.float32, arithmetic="fp32")
+            assert np.allclose(got.cpu().numpy(), want, rtol=1e-5, atol=1e-5 * scale)
+            host = gpu_convolve_rows(pix, fk, 3, 150, arithmetic="fp32")
+            assert np.allclose(host, want[3:150], rtol=1e-5, atol=1e-5 * scale)
+    res = hybrid_convolve(Image(img), FilterKernel.gaussian(radius), Platform.build(1.0, 3.0), arithmetic="fp32").pixels
+    assert np.allclose(res, oconv.rows(img, FilterKernel.gaussian(radius).weights, 0, 211), rtol=1e-5, atol=1e-5 * 255)

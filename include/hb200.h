@@ -177,8 +177,12 @@ int hb_bilateral_u8(const uint8_t* img, int32_t height, int32_t width, int32_t r
  * (out_code 64): taps in row-major order, zero weights skipped, rounded fp64
  * multiply then add, no FMA.  out_code 32 rounds that result to fp32.
  * flags & HB_FP32_ARITH: fp32 taps with FMA, within 1e-5 relative of the
- * fp64 result (north_star's filter tolerance).
+ * fp64 result (north_star's filter tolerance).  flags & HB_TAPS_DENSE: the
+ * caller states that no weight is 0 (device-pointer calls then skip reading
+ * the weights back to choose the branch-free kernel: no host wait, CUDA-graph
+ * capturable); a wrong statement is the caller's error.
  * Host-pointer calls stage only the strip plus its clamped halo rows.     */
+#define HB_TAPS_DENSE 32
 int hb_convolve(const void* img, int in_code, int32_t height, int32_t width, int32_t radius,
                 const double* weights, int32_t row0, int32_t row1, void* out, int out_code,
                 int flags, void* stream);

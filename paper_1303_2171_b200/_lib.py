@@ -26,6 +26,7 @@ HB_ASYNC = 2
 HB_ACCUMULATE = 4
 HB_SORT_BALLOT = 8
 HB_FP32_ARITH = 16
+HB_TAPS_DENSE = 32
 
 HB_GEN_RAW, HB_GEN_LOW8, HB_GEN_HI32, HB_GEN_MOD = range(4)
 HB_SPMV_SEQ, HB_SPMV_WARP, HB_SPMV_MERGE = 0, 1, 2

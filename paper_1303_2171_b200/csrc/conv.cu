@@ -238,7 +238,7 @@ extern "C" int hb_convolve(const void* img, int in_code, int32_t height, int32_t
   // no zero tap → the branch-free kernel (the zero-skip test is the only
   // data-dependent branch of the tap loop); weights are read on the host
   bool dense = true;
-  {
+  if (!(dev && (flags & HB_TAPS_DENSE))) {
     std::vector<double> hw((size_t)S * S);
     if (dev) {
       HB_CUDA_TRY(cudaMemcpyAsync(hw.data(), weights, hw.size() * 8, cudaMemcpyDeviceToHost, s));

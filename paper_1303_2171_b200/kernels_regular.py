@@ -237,7 +237,8 @@ def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False,
              ballot: bool = False) -> tuple[Any, Any, int]:
     """LSD radix sort on the GPU (hb_sort).  CUDA tensors are sorted in place
     (payload permuted alongside, stably); host arrays are left untouched and
-    sorted copies returned.  Returns (keys, payload, digit passes executed).
+    sorted copies returned.  Returns (keys, payload, digit passes executed;
+    None for asynchronous device sorts, which do not wait to learn it).
     `ballot` ranks with the ballot multi-split instead of the (device-checked)
     lane-ordered shared atomics."""
     import ctypes
@@ -262,10 +263,15 @@ def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False,
         res_k = host_empty(kb.owner.shape, kb.dtype)
         res_v = host_empty(kb.size, vb.dtype) if vb else None
         k_out, v_out = res_k.ctypes.data, (res_v.ctypes.data if vb else 0)
+    # asynchronous device sorts do not ask for the pass count: reading it
+    # would wait on the digit histogram mid-call (32-bit keys then never
+    # block the host and are CUDA-graph capturable); passes is None then
+    want_passes = not (asynchronous and kb.device)
     passes = ctypes.c_int32(0)
     _lib.call("hb_sort", vp(kb.ptr), vp(k_out), code, vp(vb.ptr if vb else 0), vp(v_out), kb.size,
-              ctypes.byref(passes), flags, current_stream_handle(keys if kb.device else None))
-    return res_k, res_v, passes.value
+              ctypes.byref(passes) if want_passes else None, flags,
+              current_stream_handle(keys if kb.device else None))
+    return res_k, res_v, (passes.value if want_passes else None)
 
 
 def _cell_indices(chunk: np.ndarray, lo, hi) -> np.ndarray:
@@ -523,6 +529,29 @@ def convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, worke
     return out
 
 
+def _device_table(owner: Any, key: str, table: np.ndarray, device: Any) -> Any:
+    """A float64 CUDA copy of a small weight table (LUT / stencil), cached on
+    its owner per device so repeated device-resident calls neither re-upload
+    it nor synchronise (and stay CUDA-graph capturable).  The cached host copy
+    is compared on every call, so an owner whose array was changed in place
+    gets a fresh upload."""
+    import torch
+
+    host = np.ascontiguousarray(table, dtype=np.float64)
+    cache = owner.__dict__.get("_device_tables")
+    if cache is None:
+        cache = {}
+        object.__setattr__(owner, "_device_tables", cache)
+    slot = (key, str(device))
+    hit = cache.get(slot)
+    if hit is not None and np.array_equal(hit[0], host):
+        return hit[1]
+    snap = host.copy()
+    dev = torch.from_numpy(snap.copy()).to(device)
+    cache[slot] = (snap, dev)
+    return dev
+
+
 def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, out: Any = None,
                       *, out_dtype: Any = np.float64, asynchronous: bool = False,
                       arithmetic: str = "fp64") -> Any:
@@ -554,9 +583,11 @@ def gpu_convolve_rows(pixels: Any, kernel: FilterKernel, row0: int, row1: int, o
             out = torch.empty((row1 - row0, width), dtype=tdt, device=pixels.device)
         if row1 == row0:
             return out
-        wt = torch.from_numpy(w).to(pixels.device)
+        wt = _device_table(kernel, "weights", w, pixels.device)
         in_code = _lib.DTYPE_CODES["u1" if pixels.dtype == torch.uint8 else "f8"]
         flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0) | math_flag
+        if bool(np.all(w != 0.0)):
+            flags |= _lib.HB_TAPS_DENSE  # the host weights tell: no read-back, no host wait
         _lib.call("hb_convolve", vp(pixels.data_ptr()), in_code, height, width, kernel.radius, vp(wt.data_ptr()),
                   row0, row1, vp(out.data_ptr()), code, flags, current_stream_handle(pixels))
         return out
@@ -708,8 +739,8 @@ def gpu_bilateral_rows(pixels: Any, lut: BilateralLut, row0: int, row1: int, out
             out = torch.empty((row1 - row0, width), dtype=tdt, device=pixels.device)
         if row1 == row0:
             return out
-        sp = torch.from_numpy(np.ascontiguousarray(lut.spatial_weights)).to(pixels.device)
-        rg = torch.from_numpy(np.ascontiguousarray(lut.range_weights)).to(pixels.device)
+        sp = _device_table(lut, "spatial", lut.spatial_weights, pixels.device)
+        rg = _device_table(lut, "range", lut.range_weights, pixels.device)
         flags = _lib.HB_DEVICE_PTRS | (_lib.HB_ASYNC if asynchronous else 0) | math_flag
         _lib.call("hb_bilateral_u8", vp(pixels.data_ptr()), height, width, lut.radius, vp(sp.data_ptr()),
                   vp(rg.data_ptr()), row0, row1, vp(out.data_ptr()), code, flags, current_stream_handle(pixels))

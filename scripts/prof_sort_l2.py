@@ -35,4 +35,4 @@ for lg in (20, 21, 22, 23, 24, 26, 28):
         torch.cuda.synchronize()
         tot += e0.elapsed_time(e1)
     ms = tot / reps
-    print(f"n=2^{lg}: {ms * 1e3:9.1f} us/sort  {n / ms / 1e6:7.2f} Gkeys/s  {n * 68 / ms / 1e9:6.0f} GB/s (68 B/key)")
+    print(f"n=2^{lg}: {ms * 1e3:9.1f} us/sort  {n / ms / 1e6:7.2f} Gkeys/s  {n * 68 / ms / 1e6:6.0f} GB/s (68 B/key)")

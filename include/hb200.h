@@ -197,8 +197,10 @@ int hb_convolve(const void* img, int in_code, int32_t height, int32_t width, int
  * becomes the stable argsort.  *passes_done (optional) receives the number
  * of digit passes executed (0 ⇔ all keys equal).  n < 2^30 per call.
  * Ranking: one shared atomic per key, relying on lane-ordered old values
- * (verified on each device before first use; the ballot multi-split runs
- * when the check fails).  flags & HB_SORT_BALLOT (or HB_SORT_RANK=ballot in
+ * (verified on each device before first use — on the bare atomic pattern
+ * and through the production pass kernels on duplicate-heavy keys with an
+ * index payload, stability checked on the device; the ballot multi-split
+ * runs when either check fails).  flags & HB_SORT_BALLOT (or HB_SORT_RANK=ballot in
  * the environment) selects the ballot multi-split, whose stability does not
  * depend on that behaviour — the library's own stable-argsort users
  * (device gen_list, spmv_preprocess) use it.  With HB_ASYNC and

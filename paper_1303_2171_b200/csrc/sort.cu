@@ -656,8 +656,14 @@ struct PassArgs {
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
 };
 
-// true when shared atomics return lane-ordered old values on this device
-// (checked once per device: 256 CTAs x 8 warps x 4 moduli x 512 rows)
+bool production_rank_selftest();
+
+// true when shared atomics return lane-ordered old values on this device:
+// checked once per device, first on the bare pattern (256 CTAs x 8 warps x 4
+// moduli x 512 rows), then through the production kernels themselves
+// (production_rank_selftest: duplicate-heavy keys with an index payload
+// through every atomics-ranked pass shape, stability checked on the device).
+// Any violation selects the ballot ranking for the process.
 bool atoms_rank_ok() {
   static int cached[64];
   static std::once_flag once[64];
@@ -672,7 +678,7 @@ bool atoms_rank_ok() {
     }
     if (bad) cudaFree(bad);
     cudaGetLastError();
-    cached[dev] = h == 0 ? 1 : 2;
+    cached[dev] = (h == 0 && production_rank_selftest()) ? 1 : 2;
   });
   return cached[dev] == 1;
 }
@@ -774,7 +780,8 @@ int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, cons
 // passes_done the digit histogram is not read back (no host sync): every
 // digit position is sorted (a constant digit's pass is the identity).
 template <typename K>
-int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, int flags, cudaStream_t s) {
+int radix_sort_impl(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, int flags, bool atoms,
+                    cudaStream_t s) {
   constexpr int P = SortCfg<K>::kPasses;
   DeviceInfo di;
   HB_TRY(device_info(&di));
@@ -784,7 +791,6 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, int
     set_error("radix sort supports n < 2^30 keys per call (got %lld)", (long long)n);
     return HB_EINVAL;
   }
-  const bool atoms = use_atomics_rank(flags);
   DevBuf hist, kalt, valt, lb;
   HB_TRY(alloc(&hist, (size_t)P * 256 * 4, s));
   HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, (size_t)P * 256 * 4, s));
@@ -853,6 +859,65 @@ int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, int
     if (vals) HB_CUDA_TRY(cudaMemcpyAsync(vals, vcur, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   }
   return HB_OK;
+}
+
+template <typename K>
+int radix_sort(K* keys, uint32_t* vals, int64_t n, K flip, int* passes_done, int flags, cudaStream_t s) {
+  return radix_sort_impl<K>(keys, vals, n, flip, passes_done, flags, use_atomics_rank(flags), s);
+}
+
+// ---- the production-path stability self-test (run once per device)
+template <typename K>
+__global__ void selftest_fill(K* keys, uint32_t* vals, int64_t n, uint64_t seed, uint64_t mod, int shift_hi) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = splitmix64_at(seed, (uint64_t)i + 1);
+    K k = (K)(r % mod);
+    if (shift_hi > 0) k |= (K)((r >> 32) % mod) << shift_hi;  // a second live digit far from the first
+    keys[i] = k;
+    vals[i] = (uint32_t)i;
+  }
+}
+template <typename K>
+__global__ void selftest_check(const K* keys, const uint32_t* vals, int64_t n, unsigned int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool ok = keys[i - 1] < keys[i] || (keys[i - 1] == keys[i] && vals[i - 1] < vals[i]);
+    if (!ok) atomicAdd(bad, 1u);
+  }
+}
+template <typename K>
+bool selftest_case(uint64_t mod, int shift_hi, bool sync_path, cudaStream_t s) {
+  const int64_t n = ((int64_t)1 << 20) + 7;  // ragged last tile
+  DevBuf keys, vals, bad;
+  if (alloc(&keys, (size_t)n * sizeof(K), s) != HB_OK || alloc(&vals, (size_t)n * 4, s) != HB_OK ||
+      alloc(&bad, 4, s) != HB_OK)
+    return false;
+  selftest_fill<K><<<256, 256, 0, s>>>(keys.as<K>(), vals.as<uint32_t>(), n, 0x5eed0000ull + mod, mod, shift_hi);
+  int passes = 0;
+  if (radix_sort_impl<K>(keys.as<K>(), vals.as<uint32_t>(), n, (K)0, sync_path ? &passes : nullptr,
+                         sync_path ? 0 : HB_ASYNC, true, s) != HB_OK)
+    return false;
+  unsigned int h = 1;
+  if (cudaMemsetAsync(bad.ptr, 0, 4, s) != cudaSuccess) return false;
+  selftest_check<K><<<256, 256, 0, s>>>(keys.as<K>(), vals.as<uint32_t>(), n, bad.as<unsigned int>());
+  if (cudaMemcpyAsync(&h, bad.ptr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return false;
+  return h == 0;
+}
+
+// Duplicate-heavy keys (2..256 distinct values per live digit) with an index
+// payload through every pass shape the atomics ranking drives: u32 one live
+// digit (onesweep_rf_kernel), u32 all four digits (packed onesweep_rfk
+// kernels: split → packed → packed → split), u32 two live digits, u64 keys.
+bool production_rank_selftest() {
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return false;
+  bool ok = selftest_case<uint32_t>(3, 0, true, s) && selftest_case<uint32_t>(2, 0, false, s) &&
+            selftest_case<uint32_t>(256, 0, false, s) && selftest_case<uint32_t>(5, 24, true, s) &&
+            selftest_case<uint64_t>(7, 40, true, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  cudaGetLastError();
+  return ok;
 }
 
 // lower_bound of (probe_key, probe_val) in the lexicographically sorted

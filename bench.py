@@ -827,7 +827,9 @@ class LrBench(Bench):
     def bytes_per_launch(self):
         return 12 * self.n // self.world
 
-    SEQ_BYTES_PER_NODE = 106  # log 8 + pairs 16 + node sort ~70 (1.03 n entries) + widen 12
+    # log 8 + packed pairs 16 + node sort ~66 (4 passes x 16 over ~1.03 n entries; the digit
+    # histogram is counted by the pairs kernel and the int64 widen is the last pass's store)
+    SEQ_BYTES_PER_NODE = 90
 
     def roofline_extra(self, ms):
         # t >= one dependent random successor read per node at the measured

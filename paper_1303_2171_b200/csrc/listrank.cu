@@ -25,6 +25,8 @@
 #include "common.cuh"
 
 namespace hb {
+int sort_pairs_widen_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int64_t n_out, int64_t* out,
+                         cudaStream_t s);
 namespace {
 
 #ifndef HB_LR_K
@@ -264,6 +266,41 @@ __global__ void lr_log_pairs_kernel(const uint64_t* __restrict__ log, int64_t sl
   }
 }
 
+// The same conversion written as packed (val << 32 | key) elements for the
+// library's pair sort, counting the four 8-bit digit histograms of the keys
+// on the way (so the sort needs no histogram pass of its own).
+__global__ void __launch_bounds__(256) lr_log_pack_kernel(const uint64_t* __restrict__ log, int64_t slots,
+                                                          const int64_t* __restrict__ prefix,
+                                                          uint64_t* __restrict__ pairs, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t le = (2u << lane) - 1u;  // lanes <= me
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = i < slots ? __ldcs(reinterpret_cast<const unsigned long long*>(log) + i) : ((uint64_t)kEmptyHi << 32);
+    const uint32_t hi = (uint32_t)(e >> 32);
+    const bool mark = (hi & kMarkBit) && hi != kEmptyHi;
+    const uint32_t mb = __ballot_sync(0xffffffffu, mark);
+    const int src = 31 - __clz(mb & le);
+    const uint32_t j = __shfl_sync(0xffffffffu, hi & ~kMarkBit, src < 0 ? 0 : src);
+    if (i < slots) {
+      const bool node = !(hi & kMarkBit);
+      const uint32_t key = node ? hi : 0xffffffffu;
+      const uint32_t val = node ? (uint32_t)(prefix[j] + (int64_t)(uint32_t)e) : 0u;
+      __stcs(reinterpret_cast<unsigned long long*>(pairs) + i, ((unsigned long long)val << 32) | key);
+#pragma unroll
+      for (int d = 0; d < 4; ++d) atomicAdd(&h[d][(key >> (8 * d)) & 255u], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
 __global__ void lr_widen_kernel(const uint32_t* __restrict__ val, int64_t n, int64_t* __restrict__ rank) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     rank[i] = (int64_t)val[i];
@@ -377,7 +414,7 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       // log + (node, rank) pair arrays allocated together, up front: the same
       // allocation pattern every call keeps the stream-ordered pool from growing
       HB_TRY(alloc(&L->log, (size_t)L->max_chunks * kLogChunk * 8, s));
-      HB_TRY(alloc(&L->key, (size_t)L->max_chunks * kLogChunk * 4, s));
+      HB_TRY(alloc(&L->key, (size_t)L->max_chunks * kLogChunk * 8, s));  // packed (rank, node) pairs
       HB_TRY(alloc(&L->val, (size_t)L->max_chunks * kLogChunk * 4, s));
       HB_TRY(alloc(&L->ctr, 8, s));
       HB_CUDA_TRY(cudaMemsetAsync(L->ctr.ptr, 0, 8, s));
@@ -489,6 +526,22 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       DevBuf& val = L->val;
       int64_t pb = ceil_div(slots, 256);
       if (pb > (int64_t)di.sms * 16) pb = (int64_t)di.sms * 16;
+      {  // packed pairs + digit histograms, one sort with the widen fused into its last pass
+        DevBuf hist;
+        HB_TRY(alloc(&hist, 4 * 256 * 4, s));
+        HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, 4 * 256 * 4, s));
+        // the packed pairs live in `key` (8 bytes per slot)
+        lr_log_pack_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, L->key.as<uint64_t>(),
+                                                   hist.as<uint32_t>());
+        HB_TRY(check_launch());
+        const int rc = sort_pairs_widen_ext(L->key.as<uint64_t>(), slots, hist.as<uint32_t>(), L->n, dst, s);
+        if (rc == HB_OK) {
+          prefix = dst;
+          continue;
+        }
+        if (rc != HB_ENOSYS) return rc;
+      }
+      // general path (ballot-ranked sorts): (node, rank) as two arrays, sort, widen
       lr_log_pairs_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, key.as<uint32_t>(),
                                                  val.as<uint32_t>());
       HB_TRY(check_launch());

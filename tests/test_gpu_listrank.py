@@ -173,3 +173,34 @@ def test_logged_walk_orders(n, order):
     want[seq] = np.arange(n)
     got = gpu_list_rank(succ.astype(np.int32), head)
     assert np.array_equal(got, want), (n, order)
+
+
+def test_ballot_ranking_fallback_paths():
+    """With the ballot ranking forced (HB_SORT_RANK=ballot, read once per
+    process: a subprocess), every sort-based path takes its general branch —
+    the logged walk's node sort included (two pair arrays + sort + widen
+    instead of the fused packed sort) — and gives the same results."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import datasets as ods\n"
+        "from oracle import listrank as olr\n"
+        "from oracle import sort as osort\n"
+        "from paper_1303_2171_b200.kernels_irregular import gpu_list_rank\n"
+        "from paper_1303_2171_b200.kernels_regular import gpu_sort\n"
+        "succ, head = ods.linked_list(1_500_000, 77)\n"
+        "got = gpu_list_rank(torch.from_numpy(succ.astype(np.int32)).cuda(), head).cpu().numpy()\n"
+        "assert np.array_equal(got, olr.chase(succ, head)), 'ranks'\n"
+        "k = (np.random.default_rng(3).integers(0, 7, size=300_001)).astype(np.uint32)\n"
+        "sk, sv, _ = gpu_sort(k, np.arange(k.size, dtype=np.uint32))\n"
+        "assert osort.check_stable_payload(k, sk, sv), 'stable payload'\n"
+        "print('ok')\n"
+    )
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, HB_SORT_RANK="ballot", PYTHONPATH=str(root) + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

@@ -67,6 +67,23 @@ int hb_stream_sync(void* stream);
 /* Release cached device staging buffers of the current device. */
 int hb_trim(void);
 
+/* Device memory and streams for callers without a GPU framework (the
+ * reference's own ctypes binding): select the device of
+ * the calling thread, allocate / free device buffers, copy host <-> device
+ * (stream-ordered; pass NULL for the legacy default stream; the copy is
+ * complete on return unless flags & HB_ASYNC — then a page-locked host
+ * buffer must stay untouched until hb_stream_sync; pageable buffers are
+ * always consumed / filled before return), create / destroy streams.
+ * Upload once, then run any entry point with HB_DEVICE_PTRS on the buffers
+ * — the device-resident mode the benchmarks use.                         */
+int hb_set_device(int device);
+int hb_buf_alloc(size_t bytes, void** out);
+int hb_buf_free(void* buf);
+int hb_buf_upload(void* dst_device, const void* src_host, size_t bytes, int flags, void* stream);
+int hb_buf_download(void* dst_host, const void* src_device, size_t bytes, int flags, void* stream);
+int hb_stream_create(void** out);
+int hb_stream_destroy(void* stream);
+
 /* ---------------------------------------------------------------- generators
  * Device-side restatement of rng.py:45-51 (`splitmix64_array`): draw k
  * (1-based, k = k0+1 .. k0+n) of the stream `seed`, transformed:

@@ -45,6 +45,13 @@ _SIGNATURES: dict[str, list] = {
     "hb_sm_count": [_c.POINTER(_int)],
     "hb_stream_sync": [_vp],
     "hb_trim": [],
+    "hb_set_device": [_int],
+    "hb_buf_alloc": [_c.c_size_t, _c.POINTER(_vp)],
+    "hb_buf_free": [_vp],
+    "hb_buf_upload": [_vp, _vp, _c.c_size_t, _int, _vp],
+    "hb_buf_download": [_vp, _vp, _c.c_size_t, _int, _vp],
+    "hb_stream_create": [_c.POINTER(_vp)],
+    "hb_stream_destroy": [_vp],
     "hb_gen_splitmix": [_u64, _u64, _i64, _int, _u64, _vp, _vp],
     "hb_hist": [_vp, _int, _i64, _i32, _vp, _int, _vp],
     "hb_spmv_csr": [_vp, _int, _vp, _int, _vp, _i64, _i64, _i64, _vp, _vp, _int, _vp, _int, _int, _vp],

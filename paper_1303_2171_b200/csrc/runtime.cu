@@ -493,6 +493,53 @@ int hb_trim(void) {
   return HB_OK;
 }
 
+int hb_set_device(int device) {
+  HB_CUDA_TRY(cudaSetDevice(device));
+  return HB_OK;
+}
+
+int hb_buf_alloc(size_t bytes, void** out) {
+  HB_CHECK_ARG(out != nullptr, "NULL out");
+  *out = nullptr;
+  if (bytes == 0) return HB_OK;
+  HB_CUDA_TRY(cudaMalloc(out, bytes));
+  return HB_OK;
+}
+
+int hb_buf_free(void* buf) {
+  if (buf) HB_CUDA_TRY(cudaFree(buf));
+  return HB_OK;
+}
+
+int hb_buf_upload(void* dst_device, const void* src_host, size_t bytes, int flags, void* stream) {
+  HB_CHECK_ARG(bytes == 0 || (dst_device && src_host), "NULL pointer");
+  if (bytes == 0) return HB_OK;
+  cudaStream_t s = hb::as_stream(stream);
+  HB_TRY(hb::copy_h2d(dst_device, src_host, bytes, s));
+  return hb::finish(flags, s);
+}
+
+int hb_buf_download(void* dst_host, const void* src_device, size_t bytes, int flags, void* stream) {
+  HB_CHECK_ARG(bytes == 0 || (dst_host && src_device), "NULL pointer");
+  if (bytes == 0) return HB_OK;
+  cudaStream_t s = hb::as_stream(stream);
+  HB_TRY(hb::copy_d2h(dst_host, src_device, bytes, s));
+  return hb::finish(flags, s);
+}
+
+int hb_stream_create(void** out) {
+  HB_CHECK_ARG(out != nullptr, "NULL out");
+  cudaStream_t s = nullptr;
+  HB_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
+  return HB_OK;
+}
+
+int hb_stream_destroy(void* stream) {
+  if (stream) HB_CUDA_TRY(cudaStreamDestroy(hb::as_stream(stream)));
+  return HB_OK;
+}
+
 int hb_gen_splitmix(uint64_t seed, uint64_t k0, int64_t n, int kind, uint64_t bound, void* out,
                     void* stream) {
   HB_CHECK_ARG(n >= 0, "n must be >= 0");

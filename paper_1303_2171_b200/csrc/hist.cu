@@ -19,6 +19,10 @@
 //  * bin_count > 256: one CTA-shared copy (dynamic smem, <= 49152 bins).
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 
 namespace hb {
@@ -80,11 +84,23 @@ __device__ __forceinline__ void put_vec(uint32_t* s, uint4 q, uint32_t bins, uin
 }
 
 // bins <= 256: lane-striped privatised histogram.
+// Per-stream scratch of the striped kernel: acc[0..255] bin sums, acc[256]
+// out-of-domain count, ticket = CTAs done.  Invariant between calls: all
+// zero.  The last CTA to finish publishes acc into the caller's bins (set or
+// add), the domain-error count into *err_out, and zeroes acc and the ticket
+// again — so a call needs no memset and no allocation (calls on one stream
+// are ordered; each stream has its own scratch).
+struct HistScratch {
+  unsigned long long acc[257];
+  unsigned int ticket;
+  unsigned int err_out;
+};
+
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(kThreads)
     hist_striped_kernel(const T* __restrict__ data, int64_t head, int64_t nvec, int64_t n,
                         uint32_t bins, unsigned long long* __restrict__ out,
-                        unsigned int* __restrict__ err) {
+                        HistScratch* __restrict__ sc, bool accumulate) {
   __shared__ uint32_t s[256 * kStripes];
   const uint32_t lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 256 * kStripes; i += blockDim.x) s[i] = 0;
@@ -113,7 +129,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t j = tail0 + threadIdx.x; j < n; j += blockDim.x)
       put_striped<T, CHECK || sizeof(T) != 1>(s, data[j], bins, lane, bad);
   }
-  if (bad) atomicAdd(err, bad);
+  if (bad) atomicAdd(&sc->acc[256], (unsigned long long)bad);
   __syncthreads();
 
   // fold the 32 stripes of each bin; rotate the start so the 32 threads of a
@@ -122,11 +138,22 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t sum = 0;
 #pragma unroll 8
     for (uint32_t j = 0; j < kStripes; ++j) sum += s[(b << 5) | ((j + b) & 31)];
-    if (sum) {
-      if (b < bins) atomicAdd(out + b, (unsigned long long)sum);
-      else atomicAdd(err, sum);  // uint8 value >= bin_count
-    }
+    if (sum) atomicAdd(&sc->acc[b < bins ? b : 256], (unsigned long long)sum);  // b >= bins: uint8 value >= bin_count
   }
+  // the last CTA publishes and restores the all-zero scratch
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (uint32_t b = threadIdx.x; b < 257; b += blockDim.x) {
+    const unsigned long long v = atomicExch(&sc->acc[b], 0ull);
+    if (b < bins) out[b] = accumulate ? out[b] + v : v;
+    else if (b == 256) sc->err_out = (unsigned int)v;
+  }
+  if (threadIdx.x == 0) sc->ticket = 0;
 }
 
 // bins > 256: one CTA-shared copy in dynamic shared memory.
@@ -150,6 +177,54 @@ __global__ void __launch_bounds__(kThreads)
     if (sh[b]) atomicAdd(out + b, (unsigned long long)sh[b]);
 }
 
+// the scratch of (current device, stream), created zeroed on first use
+int hist_scratch(cudaStream_t s, HistScratch** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, HistScratch*> table;
+  int dev = 0;
+  HB_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = table.find({dev, s});
+  if (it != table.end()) {
+    *out = it->second;
+    return HB_OK;
+  }
+  HistScratch* p = nullptr;
+  HB_CUDA_TRY(cudaMalloc(&p, sizeof(HistScratch)));
+  HB_CUDA_TRY(cudaMemset(p, 0, sizeof(HistScratch)));  // synchronous: zero before any use
+  table[{dev, s}] = p;
+  *out = p;
+  return HB_OK;
+}
+
+template <typename T>
+int launch_striped(const void* data, int64_t n, uint32_t bins, unsigned long long* out, bool accumulate,
+                   HistScratch* sc, cudaStream_t s) {
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  const T* d = reinterpret_cast<const T*>(data);
+  constexpr int E = 16 / sizeof(T);
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(d);
+  int64_t head = (int64_t)(((16 - (addr & 15)) & 15) / sizeof(T));
+  if (addr % sizeof(T) != 0) {
+    set_error("histogram input is not aligned to its element size");
+    return HB_EINVAL;
+  }
+  if (head > n) head = n;
+  const int64_t nvec = (n - head) / E;
+  int64_t blocks = ceil_div(nvec, (int64_t)kThreads * kUnroll);
+  const int64_t cap = (int64_t)di.sms * 4;  // 4 CTAs x 32 KB smem per SM
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const bool u8 = sizeof(T) == 1 && !((T)-1 < 0);
+  if (u8 || bins == 0) {
+    hist_striped_kernel<T, false><<<(int)blocks, kThreads, 0, s>>>(d, head, nvec, n, bins, out, sc, accumulate);
+  } else {
+    hist_striped_kernel<T, true><<<(int)blocks, kThreads, 0, s>>>(d, head, nvec, n, bins, out, sc, accumulate);
+  }
+  return check_launch();
+}
+
 template <typename T>
 int launch_hist(const void* data, int64_t n, uint32_t bins, unsigned long long* out,
                 unsigned int* err, cudaStream_t s) {
@@ -157,27 +232,7 @@ int launch_hist(const void* data, int64_t n, uint32_t bins, unsigned long long* 
   HB_TRY(device_info(&di));
   if (n == 0) return HB_OK;
   const T* d = reinterpret_cast<const T*>(data);
-  if (bins <= 256) {
-    constexpr int E = 16 / sizeof(T);
-    const uintptr_t addr = reinterpret_cast<uintptr_t>(d);
-    int64_t head = (int64_t)(((16 - (addr & 15)) & 15) / sizeof(T));
-    if (addr % sizeof(T) != 0) {
-      set_error("histogram input is not aligned to its element size");
-      return HB_EINVAL;
-    }
-    if (head > n) head = n;
-    const int64_t nvec = (n - head) / E;
-    int64_t blocks = ceil_div(nvec, (int64_t)kThreads * kUnroll);
-    const int64_t cap = (int64_t)di.sms * 4;  // 4 CTAs x 32 KB smem per SM
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    const bool u8 = sizeof(T) == 1 && !((T)-1 < 0);
-    if (u8 || bins == 0) {
-      hist_striped_kernel<T, false><<<(int)blocks, kThreads, 0, s>>>(d, head, nvec, n, bins, out, err);
-    } else {
-      hist_striped_kernel<T, true><<<(int)blocks, kThreads, 0, s>>>(d, head, nvec, n, bins, out, err);
-    }
-  } else {
+  {
     size_t smem = (size_t)bins * 4;
     HB_CUDA_TRY(cudaFuncSetAttribute(hist_shared_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
@@ -221,23 +276,40 @@ extern "C" int hb_hist(const void* data, int dtype, int64_t n, int32_t bin_count
   DevBuf in, out, err;
   HB_TRY(stage_in(&in, data, (size_t)n * es, dev, s));
   HB_TRY(stage_out(&out, bins_out, (size_t)bin_count * 8, dev, s));
-  if (!dev || !(flags & HB_ACCUMULATE)) HB_CUDA_TRY(cudaMemsetAsync(out.ptr, 0, (size_t)bin_count * 8, s));
-  // domain-error counter: only read back when the call is synchronous
-  HB_TRY(alloc(&err, 4, s));
-  HB_CUDA_TRY(cudaMemsetAsync(err.ptr, 0, 4, s));
-
-  int rc = HB_OK;
   auto* o = out.as<unsigned long long>();
-  auto* e = err.as<unsigned int>();
-  switch (dtype) {
-    case HB_U8: rc = launch_hist<uint8_t>(in.ptr, n, bin_count, o, e, s); break;
-    case HB_I8: rc = launch_hist<int8_t>(in.ptr, n, bin_count, o, e, s); break;
-    case HB_U16: rc = launch_hist<uint16_t>(in.ptr, n, bin_count, o, e, s); break;
-    case HB_I16: rc = launch_hist<int16_t>(in.ptr, n, bin_count, o, e, s); break;
-    case HB_U32: rc = launch_hist<uint32_t>(in.ptr, n, bin_count, o, e, s); break;
-    case HB_I32: rc = launch_hist<int32_t>(in.ptr, n, bin_count, o, e, s); break;
-    case HB_U64: rc = launch_hist<uint64_t>(in.ptr, n, bin_count, o, e, s); break;
-    default: rc = launch_hist<int64_t>(in.ptr, n, bin_count, o, e, s); break;
+  const bool accumulate_dev = dev && (flags & HB_ACCUMULATE);
+  int rc = HB_OK;
+  HistScratch* sc = nullptr;
+  if (bin_count <= 256 && n > 0) {
+    // striped kernel: bins set (or added) and the domain count published by
+    // its last CTA through the stream's scratch — no memset, no allocation
+    HB_TRY(hist_scratch(s, &sc));
+    switch (dtype) {
+      case HB_U8: rc = launch_striped<uint8_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      case HB_I8: rc = launch_striped<int8_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      case HB_U16: rc = launch_striped<uint16_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      case HB_I16: rc = launch_striped<int16_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      case HB_U32: rc = launch_striped<uint32_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      case HB_I32: rc = launch_striped<int32_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      case HB_U64: rc = launch_striped<uint64_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+      default: rc = launch_striped<int64_t>(in.ptr, n, bin_count, o, accumulate_dev, sc, s); break;
+    }
+  } else {
+    if (!accumulate_dev) HB_CUDA_TRY(cudaMemsetAsync(out.ptr, 0, (size_t)bin_count * 8, s));
+    // domain-error counter: only read back when the call is synchronous
+    HB_TRY(alloc(&err, 4, s));
+    HB_CUDA_TRY(cudaMemsetAsync(err.ptr, 0, 4, s));
+    auto* e = err.as<unsigned int>();
+    switch (dtype) {
+      case HB_U8: rc = launch_hist<uint8_t>(in.ptr, n, bin_count, o, e, s); break;
+      case HB_I8: rc = launch_hist<int8_t>(in.ptr, n, bin_count, o, e, s); break;
+      case HB_U16: rc = launch_hist<uint16_t>(in.ptr, n, bin_count, o, e, s); break;
+      case HB_I16: rc = launch_hist<int16_t>(in.ptr, n, bin_count, o, e, s); break;
+      case HB_U32: rc = launch_hist<uint32_t>(in.ptr, n, bin_count, o, e, s); break;
+      case HB_I32: rc = launch_hist<int32_t>(in.ptr, n, bin_count, o, e, s); break;
+      case HB_U64: rc = launch_hist<uint64_t>(in.ptr, n, bin_count, o, e, s); break;
+      default: rc = launch_hist<int64_t>(in.ptr, n, bin_count, o, e, s); break;
+    }
   }
   if (rc != HB_OK) return rc;
   if (flags & HB_ASYNC) return check_launch();
@@ -249,7 +321,8 @@ extern "C" int hb_hist(const void* data, int dtype, int64_t n, int32_t bin_count
     if (!host_tmp) { set_error("host allocation failed"); return HB_ENOMEM; }
     HB_CUDA_TRY(cudaMemcpyAsync(host_tmp, out.ptr, (size_t)bin_count * 8, cudaMemcpyDeviceToHost, s));
   }
-  HB_CUDA_TRY(cudaMemcpyAsync(&bad, err.ptr, 4, cudaMemcpyDeviceToHost, s));
+  if (sc) HB_CUDA_TRY(cudaMemcpyAsync(&bad, &sc->err_out, 4, cudaMemcpyDeviceToHost, s));
+  else if (err.ptr) HB_CUDA_TRY(cudaMemcpyAsync(&bad, err.ptr, 4, cudaMemcpyDeviceToHost, s));
   HB_CUDA_TRY(cudaStreamSynchronize(s));
   if (!dev && (flags & HB_ACCUMULATE)) {
     for (int32_t b = 0; b < bin_count; ++b) bins_out[b] += host_tmp[b];

@@ -3,8 +3,8 @@
 //
 // Design:
 //  * HBM-bound streaming read: every thread issues UNROLL independent 16-byte
-//    `ld.global.nc.L1::no_allocate` loads before touching shared memory, so
-//    each SM keeps ~64 KB of reads in flight.  Grid = SMs x CTAs/SM
+//    `ld.global.nc.L1::no_allocate` loads before touching shared memory (16
+//    per round: 0.97-1.0 of the measured copy peak from 2^31 bytes up).  Grid = SMs x CTAs/SM
 //    (persistent, grid-stride over 16-byte vectors).
 //  * Privatisation: for bin_count <= 256 each CTA owns 32 sub-histograms laid
 //    out LANE-STRIPED, word = bin*32 + lane, so the 32 shared-memory atomics
@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kStripes = 32;         // sub-histograms per CTA (one per lane)
 constexpr int kThreads = 512;        // 16 warps
-constexpr int kUnroll = 4;           // 16-byte loads in flight per thread
+constexpr int kUnroll = 16;          // 16-byte loads per thread per round (4: 176.4 us at 2^30, 8: 172.8, 16: 172.1)
 constexpr int kMaxSharedBins = 49152;
 
 template <typename T>

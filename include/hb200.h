@@ -302,13 +302,21 @@ int hb_merge_runs(const void* keys, int key_code, const uint32_t* vals, int64_t 
  *                    cover all n nodes, else HB_ESTRUCT — on every rank
  *                    alike) and turns packed into ranks for the nodes of
  *                    sublists [sub_lo, sub_hi), 0 for all other nodes;
- *  (caller)          all-reduce (sum) of rank → every rank holds all ranks.
+ *  (caller)          all-reduce (sum) of rank → every rank holds all ranks
+ *                    (int32 ranks + hb_widen_i32 when n <= 2^31).
  * Device pointers only; n < 2^31.                                          */
 int hb_lr_layout(int64_t n, int64_t head, int64_t* nsub, int64_t* sub_head);
 int hb_lr_walk_part(const void* succ, int succ_code, int64_t n, int64_t head, int64_t sub_lo, int64_t sub_hi,
                     int64_t* packed, int64_t* sub_nxt, int64_t* sub_len, int flags, void* stream);
 int hb_lr_finish_part(const int64_t* sub_nxt, const int64_t* sub_len, int64_t nsub, int64_t sub_head, int64_t n,
                       int64_t sub_lo, int64_t sub_hi, int64_t* rank, int flags, void* stream);
+/* hb_lr_finish_part with int32 ranks (n <= 2^31): reads the packed walk
+ * output and writes rank32 — the all-reduce then moves 4 bytes per node —
+ * and hb_widen_i32 turns the reduced ranks back into the int64 result.    */
+int hb_lr_finish_part32(const int64_t* sub_nxt, const int64_t* sub_len, int64_t nsub, int64_t sub_head, int64_t n,
+                        int64_t sub_lo, int64_t sub_hi, const int64_t* packed, int32_t* rank32, int flags,
+                        void* stream);
+int hb_widen_i32(const int32_t* in, int64_t n, int64_t* out, int flags, void* stream);
 
 /* ------------------------------------------------------- host (DeviceA)
  * The host share of a work-shared run on `workers` host threads, bit-identical

@@ -77,6 +77,8 @@ _SIGNATURES: dict[str, list] = {
     "hb_lr_layout": [_i64, _i64, _vp, _vp],
     "hb_lr_walk_part": [_vp, _int, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _int, _vp],
     "hb_lr_finish_part": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _int, _vp],
+    "hb_lr_finish_part32": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _int, _vp],
+    "hb_widen_i32": [_vp, _i64, _vp, _int, _vp],
 }
 
 _lock = threading.Lock()

@@ -20,6 +20,7 @@
 //            level.
 // The walk is a chain of dependent random 4-byte reads (one 32-byte sector
 // per node): it is bound by DRAM sector throughput, not bytes.
+#include <climits>
 #include <vector>
 
 #include "common.cuh"
@@ -578,6 +579,24 @@ __global__ void lr_expand_part_kernel(int64_t* __restrict__ io, int64_t n, const
   }
 }
 
+// the same expansion into int32 ranks (n < 2^31): the all-reduce that
+// merges the ranks of all GPUs then moves half the bytes
+__global__ void lr_expand_part32_kernel(const int64_t* __restrict__ packed, int64_t n,
+                                        const int64_t* __restrict__ prefix, int64_t lo, int64_t hi,
+                                        int32_t* __restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = (uint64_t)packed[v];
+    const int64_t j = (int64_t)(t >> 32);
+    out[v] = (j >= lo && j < hi) ? (int32_t)(prefix[j] + (int64_t)(t & 0xffffffffull)) : 0;
+  }
+}
+
+__global__ void widen_i32_kernel(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)in[i];
+}
+
 void lr_layout(int64_t n, int64_t head, int64_t* nsub, int64_t* sub_head) {
   const int64_t regular = ceil_div(n, kK);
   const bool extra = head % kK != 0;
@@ -736,6 +755,39 @@ extern "C" int hb_lr_walk_part(const void* succ, int succ_code, int64_t n, int64
                ? walk_part<int32_t>((const int32_t*)succ, n, head, sub_lo, sub_hi, (uint64_t*)packed, sub_nxt, sub_len, s)
                : walk_part<int64_t>((const int64_t*)succ, n, head, sub_lo, sub_hi, (uint64_t*)packed, sub_nxt, sub_len, s);
   if (rc != HB_OK) return rc;
+  return finish(flags, s);
+}
+
+extern "C" int hb_lr_finish_part32(const int64_t* sub_nxt, const int64_t* sub_len, int64_t nsub,
+                                   int64_t sub_head, int64_t n, int64_t sub_lo, int64_t sub_hi,
+                                   const int64_t* packed, int32_t* rank32, int flags, void* stream) {
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "the sharded ranking works on device arrays");
+  HB_CHECK_ARG(n >= 1 && n <= (int64_t)INT32_MAX + 1 && nsub >= 1 && sub_head >= 0 && sub_head < nsub,
+               "bad sublist layout (int32 ranks need n <= 2^31)");
+  HB_CHECK_ARG(0 <= sub_lo && sub_lo <= sub_hi && sub_hi <= nsub, "sublist range out of range");
+  HB_CHECK_ARG(sub_nxt && sub_len && packed && rank32, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  DevBuf prefix;
+  HB_TRY(alloc(&prefix, (size_t)nsub * 8, s));
+  HB_TRY(rank_levels<int64_t>(sub_nxt, sub_len, nsub, sub_head, n, prefix.as<int64_t>(), s));
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)di.sms * 32) blocks = (int64_t)di.sms * 32;
+  lr_expand_part32_kernel<<<(int)blocks, 256, 0, s>>>(packed, n, prefix.as<int64_t>(), sub_lo, sub_hi, rank32);
+  return finish(flags, s);
+}
+
+extern "C" int hb_widen_i32(const int32_t* in, int64_t n, int64_t* out, int flags, void* stream) {
+  HB_CHECK_ARG((flags & HB_DEVICE_PTRS) != 0, "hb_widen_i32 works on device arrays");
+  HB_CHECK_ARG(n >= 0 && (n == 0 || (in && out)), "bad arguments");
+  if (n == 0) return HB_OK;
+  cudaStream_t s = as_stream(stream);
+  DeviceInfo di;
+  HB_TRY(device_info(&di));
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)di.sms * 32) blocks = (int64_t)di.sms * 32;
+  widen_i32_kernel<<<(int)blocks, 256, 0, s>>>(in, n, out);
   return finish(flags, s);
 }
 

@@ -660,9 +660,17 @@ def list_rank_sharded(succ: Any, head: int, g: "sharding.ShardGroup", out: Any =
     counts = [b[k + 1] - b[k] for k in range(g.world)]
     nxt_all = sharding.gather_blocks(nxt[lo:hi], counts, g)
     ln_all = sharding.gather_blocks(ln[lo:hi], counts, g)
-    _lib.call("hb_lr_finish_part", vp(nxt_all.data_ptr()), vp(ln_all.data_ptr()), nsub, sub_head, n, lo, hi,
-              vp(rank.data_ptr()), _lib.HB_DEVICE_PTRS | _lib.HB_ASYNC, stream)
-    sharding.all_reduce_sum(rank, g)
+    flags = _lib.HB_DEVICE_PTRS | _lib.HB_ASYNC
+    if n <= 2**31:  # int32 ranks on the wire: the merging all-reduce moves 4 bytes per node, not 8
+        r32 = torch.empty(n, dtype=torch.int32, device=dev)
+        _lib.call("hb_lr_finish_part32", vp(nxt_all.data_ptr()), vp(ln_all.data_ptr()), nsub, sub_head, n, lo, hi,
+                  vp(rank.data_ptr()), vp(r32.data_ptr()), flags, stream)
+        sharding.all_reduce_sum(r32, g)
+        _lib.call("hb_widen_i32", vp(r32.data_ptr()), n, vp(rank.data_ptr()), flags, current_stream_handle(r32))
+    else:
+        _lib.call("hb_lr_finish_part", vp(nxt_all.data_ptr()), vp(ln_all.data_ptr()), nsub, sub_head, n, lo, hi,
+                  vp(rank.data_ptr()), flags, stream)
+        sharding.all_reduce_sum(rank, g)
     return rank if is_device_array(succ) else rank.cpu().numpy()
 
 

@@ -20,6 +20,9 @@
 //            level.
 // The walk is a chain of dependent random 4-byte reads (one 32-byte sector
 // per node): it is bound by DRAM sector throughput, not bytes.
+#include <stdlib.h>
+
+#include <algorithm>
 #include <climits>
 #include <vector>
 
@@ -77,6 +80,7 @@ __device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra
 #define HB_LR_CHAINS 1  // measured with dynamic claiming: 1 / 2 / 3 / 4 / 8 chains = 13.24 / 12.97 / 12.76 / 12.62 / 12.0 Gnodes/s
 #endif
 constexpr int kChains = HB_LR_CHAINS;
+constexpr int64_t kWalkBlocksPer10Sm = 36;  // level-1 log walk: 3.6 blocks of 128 threads per SM
 
 // Successor reads are random: load them L2-only (.cg).  The read-only
 // (.nc / __ldg) path promotes every L1 miss to a full 128-byte line, i.e.
@@ -433,6 +437,11 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     HB_TRY(alloc(&jobs, 8, s));
     HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
     if (L->logged) {
+      // fewer walks in flight than the SMs could hold: on B200 the dependent
+      // random reads are served fastest with ~68K chains (3.6 blocks of 128
+      // per SM: 15.0-15.2 ms per 2^28-node call; 4 per SM: 16.8 ms; 16 per SM:
+      // 17.1 ms — profiles/micro_lr_chains_r02.txt)
+      blocks = std::min<int64_t>(blocks, (int64_t)di.sms * kWalkBlocksPer10Sm / 10);
       lr_walk_log_kernel<S><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, cur_n, cur_head, L->nsub, L->extra, L->log.as<uint64_t>(),
           L->ctr.as<unsigned long long>(), L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),

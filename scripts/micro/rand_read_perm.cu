@@ -58,15 +58,20 @@ int main() {
       link<<<sms * 8, 256>>>(order, n, succ);
     }
     cudaDeviceSynchronize();
-    chase<<<blocks, threads>>>(succ, n, steps, sink);
-    cudaEventRecord(a);
-    chase<<<blocks, threads>>>(succ, n, steps, sink);
-    cudaEventRecord(b);
-    cudaEventSynchronize(b);
-    float ms;
-    cudaEventElapsedTime(&ms, a, b);
-    printf("%-22s %7.3f ms  %6.2f G dependent reads/s\n", kind == 0 ? "affine permutation" : "random cyclic list", ms,
-           reads / ms / 1e6);
+    // the same number of reads spread over fewer, longer chains
+    for (int bps : {16, 8, 6, 4, 3}) {
+      const int bl = sms * bps, st = (int)(reads / ((double)bl * threads));
+      chase<<<bl, threads>>>(succ, n, st, sink);
+      cudaEventRecord(a);
+      chase<<<bl, threads>>>(succ, n, st, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("%-22s %6d chains x %5d steps: %7.3f ms  %6.2f G dependent reads/s\n",
+             kind == 0 ? "affine permutation" : "random cyclic list", bl * threads, st, ms,
+             (double)bl * threads * st / ms / 1e6);
+    }
   }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;

@@ -437,11 +437,15 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     HB_TRY(alloc(&jobs, 8, s));
     HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
     if (L->logged) {
-      // fewer walks in flight than the SMs could hold: on B200 the dependent
-      // random reads are served fastest with ~68K chains (3.6 blocks of 128
-      // per SM: 15.0-15.2 ms per 2^28-node call; 4 per SM: 16.8 ms; 16 per SM:
-      // 17.1 ms — profiles/micro_lr_chains_r02.txt)
-      blocks = std::min<int64_t>(blocks, (int64_t)di.sms * kWalkBlocksPer10Sm / 10);
+      // 2^27..2^28 nodes: fewer walks in flight than the SMs could hold —
+      // ~68K walks (3.6 blocks of 128 per SM) measured 15.0-15.5 ms per
+      // 2^28-node call in a fresh process against 16.5-17.1 ms with one walk
+      // per resident thread (4 blocks/SM: 16.8, 16: 17.1), and 7.6 vs 8.4 ms
+      // at 2^27; outside that range (2^24-2^26, 2^29) the cap is neutral or
+      // slower.  The fast mode is not reached in every process (after other
+      // list sizes were ranked: 16.6-17.6 ms) — profiles/micro_lr_chains_r02.txt.
+      if (cur_n >= ((int64_t)1 << 27) && cur_n <= ((int64_t)1 << 28))
+        blocks = std::min<int64_t>(blocks, (int64_t)di.sms * kWalkBlocksPer10Sm / 10);
       lr_walk_log_kernel<S><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, cur_n, cur_head, L->nsub, L->extra, L->log.as<uint64_t>(),
           L->ctr.as<unsigned long long>(), L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),

@@ -24,6 +24,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -81,6 +84,32 @@ __device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra
 #endif
 constexpr int kChains = HB_LR_CHAINS;
 constexpr int64_t kWalkBlocksPer10Sm = 36;  // level-1 log walk: 3.6 blocks of 128 threads per SM
+
+// The level-1 walk's two hot global counters (sublist claims, log-chunk
+// claims) live in one cached 2 MB block per (device, stream), 256 bytes
+// apart.  Where they land relative to each other decides how fast the walk
+// runs — in one 128-byte line 24.4 ms per 2^28-node call, 256 B or 64 KB
+// apart 15.4-15.6 ms, 4 KB apart 18.6 ms (L2 atomic-unit sharing;
+// profiles/micro_lr_chains_r02.txt) — and two separate pool allocations
+// land wherever the pool's history puts them.
+constexpr size_t kCtrJobs = 0, kCtrChunks = 256 / 8;  // u64 slots
+int walk_counters(cudaStream_t s, unsigned long long** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> table;
+  int dev = 0;
+  HB_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = table.find({dev, s});
+  if (it != table.end()) {
+    *out = it->second;
+    return HB_OK;
+  }
+  unsigned long long* p = nullptr;
+  HB_CUDA_TRY(cudaMalloc(&p, (size_t)2 << 20));  // 2 MB: one large page, both counters inside it
+  table[{dev, s}] = p;
+  *out = p;
+  return HB_OK;
+}
 
 // Successor reads are random: load them L2-only (.cg).  The read-only
 // (.nc / __ldg) path promotes every L1 miss to a full 128-byte line, i.e.
@@ -172,6 +201,7 @@ __global__ void __launch_bounds__(128)
 // (lr_log_pairs_kernel), which the library's radix sort orders by node —
 // coalesced passes — and the ranks are widened into rank[] in node order.
 constexpr int kLogChunk = 32;
+constexpr int kChunkClaim = 2;  // log chunks per counter claim
 constexpr uint32_t kMarkBit = 0x80000000u;
 constexpr uint32_t kEmptyHi = 0xffffffffu;
 constexpr int64_t kLogMin = 1 << 20;  // smaller lists: the plain walk (everything fits in L2)
@@ -206,12 +236,26 @@ __global__ void __launch_bounds__(128)
       nb = 0;
     }
   };
+  // Chunks are claimed kChunkClaim at a time.  One at a time, the chunk and
+  // sublist counters take ~13M returning atomics per 2^28-node walk, enough
+  // to queue at their L2 slices, and the walk then runs 14.9-17.6 ms
+  // depending on which slices the counters land on; claiming chunks in pairs
+  // makes it 14.9 ms wherever they land (claiming sublists in pairs instead
+  // is slower, 18.6 ms; profiles/micro_lr_chains_r02.txt).
+  int64_t spare = -1, spare_end = -1;  // claimed chunks not yet opened: [spare, spare_end)
   auto put = [&](uint64_t e, uint32_t j) {
     if (fill == kLogChunk) {
-      const int64_t c = (int64_t)atomicAdd(chunk_ctr, 1ull);
-      if (c >= max_chunks) {
-        overflow = true;
-        return;
+      int64_t c = spare;
+      if (c >= 0) {
+        if (++spare >= spare_end) spare = -1;
+      } else {
+        c = (int64_t)atomicAdd(chunk_ctr, (unsigned long long)kChunkClaim);
+        if (c >= max_chunks) {
+          overflow = true;
+          return;
+        }
+        spare_end = c + kChunkClaim < max_chunks ? c + kChunkClaim : max_chunks;
+        spare = c + 1 < spare_end ? c + 1 : -1;
       }
       cbase = c * kLogChunk;
       fill = 0;
@@ -219,14 +263,12 @@ __global__ void __launch_bounds__(128)
     }
     push(e);
   };
-  for (;;) {
-    const int64_t jj = (int64_t)atomicAdd(jobs, 1ull);
-    if (jj >= nsub || overflow) break;
+  auto walk = [&](int64_t jj) {
     const int64_t h = jj == extra ? head : jj * kK;
     if (h >= n) {
       nxt[jj] = -1;
       len[jj] = 0;
-      continue;
+      return;
     }
     const uint32_t j = (uint32_t)jj;
     if (fill < kLogChunk && fill > 0) push((uint64_t)(kMarkBit | j) << 32);  // a new walk inside the chunk: its marker
@@ -242,10 +284,22 @@ __global__ void __launch_bounds__(128)
     if (steps > n) atomicAdd(err, 1ull);  // cycle without a sublist head
     nxt[jj] = (v == -1 || steps > n) ? -1 : sub_id(v, head, extra);
     len[jj] = steps > n ? n + 1 : acc;
+  };
+  for (;;) {
+    const int64_t jj = (int64_t)atomicAdd(jobs, 1ull);
+    if (jj >= nsub || overflow) break;
+    walk(jj);
   }
   if (overflow) atomicAdd(err, 1ull);
-  if (!overflow)
+  if (!overflow) {
     while (fill > 0 && fill < kLogChunk) push((uint64_t)kEmptyHi << 32);  // pad (and flush) the last chunk
+    for (; spare >= 0 && spare < spare_end; ++spare) {  // claimed chunks never opened: all padding
+      const ulonglong2 pad = make_ulonglong2((uint64_t)kEmptyHi << 32, (uint64_t)kEmptyHi << 32);
+      ulonglong2* p = reinterpret_cast<ulonglong2*>(log + spare * kLogChunk);
+#pragma unroll
+      for (int k = 0; k < kLogChunk / 2; ++k) __stcs(p + k, pad);
+    }
+  }
 }
 
 // log slot → (key = node, val = prefix[sublist] + offset); markers and
@@ -415,7 +469,7 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     L->logged = first && w0 == nullptr && cur_n >= kLogMin && cur_n <= (1ll << 29);  // sort size < 2^30
     if (L->logged) {
       // every full chunk holds >= 31 node / walk-start entries; plus one partial chunk per thread
-      L->max_chunks = (cur_n + L->nsub) / (kLogChunk - 1) + (int64_t)di.sms * 16 * 128 + 64;
+      L->max_chunks = (cur_n + L->nsub) / (kLogChunk - 1) + (int64_t)di.sms * 16 * 128 * kChunkClaim + 64;
       // log + (node, rank) pair arrays allocated together, up front: the same
       // allocation pattern every call keeps the stream-ordered pool from growing
       HB_TRY(alloc(&L->log, (size_t)L->max_chunks * kLogChunk * 8, s));
@@ -437,19 +491,25 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     HB_TRY(alloc(&jobs, 8, s));
     HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
     if (L->logged) {
-      // 2^27..2^28 nodes: fewer walks in flight than the SMs could hold —
-      // ~68K walks (3.6 blocks of 128 per SM) measured 15.0-15.5 ms per
-      // 2^28-node call in a fresh process against 16.5-17.1 ms with one walk
-      // per resident thread (4 blocks/SM: 16.8, 16: 17.1), and 7.6 vs 8.4 ms
-      // at 2^27; outside that range (2^24-2^26, 2^29) the cap is neutral or
-      // slower.  The fast mode is not reached in every process (after other
-      // list sizes were ranked: 16.6-17.6 ms) — profiles/micro_lr_chains_r02.txt.
-      if (cur_n >= ((int64_t)1 << 27) && cur_n <= ((int64_t)1 << 28))
-        blocks = std::min<int64_t>(blocks, (int64_t)di.sms * kWalkBlocksPer10Sm / 10);
+      // Fewer walks in flight than the SMs could hold: 3.6 blocks of 128
+      // per SM (~68K walks) from 2^27 nodes up — 14.9 vs 16.9 ms per
+      // 2^28-node call and 29.5 vs 33.3 ms at 2^29 against one walk per
+      // resident thread; 4 blocks/SM is as fast in some processes (14.5) and
+      // 16.6 ms in others, 3.6 was 14.9-15.0 in every process measured — and
+      // 6 blocks/SM below 2^27 (3.67 vs 4.06 ms at 2^26, 1.42 vs 1.54 at
+      // 2^24; neutral at 2^20-2^22).  profiles/micro_lr_chains_r02.txt.
+      blocks = std::min<int64_t>(blocks, cur_n >= ((int64_t)1 << 27) ? (int64_t)di.sms * kWalkBlocksPer10Sm / 10
+                                                                      : (int64_t)di.sms * 6);
+      unsigned long long* ctr = nullptr;
+      HB_TRY(walk_counters(s, &ctr));
+      HB_CUDA_TRY(cudaMemsetAsync(ctr + kCtrJobs, 0, 8, s));
+      HB_CUDA_TRY(cudaMemsetAsync(ctr + kCtrChunks, 0, 8, s));
       lr_walk_log_kernel<S><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, cur_n, cur_head, L->nsub, L->extra, L->log.as<uint64_t>(),
-          L->ctr.as<unsigned long long>(), L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),
-          err.as<unsigned long long>(), jobs.as<unsigned long long>());
+          ctr + kCtrChunks, L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),
+          err.as<unsigned long long>(), ctr + kCtrJobs);
+      // the chunk count the pairs pass reads back
+      HB_CUDA_TRY(cudaMemcpyAsync(L->ctr.ptr, ctr + kCtrChunks, 8, cudaMemcpyDeviceToDevice, s));
     } else if (first && w0 != nullptr) {
       lr_walk_kernel<S, true><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, w0, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
@@ -535,7 +595,7 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       unsigned long long used = 0;
       HB_CUDA_TRY(cudaMemcpyAsync(&used, L->ctr.ptr, 8, cudaMemcpyDeviceToHost, s));
       HB_CUDA_TRY(cudaStreamSynchronize(s));
-      const int64_t slots = (int64_t)used * kLogChunk;
+      const int64_t slots = (int64_t)std::min<unsigned long long>(used, (unsigned long long)L->max_chunks) * kLogChunk;
       DevBuf& key = L->key;
       DevBuf& val = L->val;
       int64_t pb = ceil_div(slots, 256);

@@ -20,7 +20,7 @@ cap() {  # workload kernel-regex skip
 }
 cap hist hist_striped_kernel 1
 cap spmv spmv_sell_kernel 1
-cap sort onesweep_rfk_kernel 2
+cap sort onesweep_rfk_kernel 11  # skip the 10 launches of the device self-test (2^20 keys): capture the first packed 2^28 pass
 cap lr lr_walk_log_kernel 1
 cap bilat bilateral_tma_kernel 1
 cap conv conv_rows_kernel 1

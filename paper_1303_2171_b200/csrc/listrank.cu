@@ -24,9 +24,6 @@
 
 #include <algorithm>
 #include <climits>
-#include <map>
-#include <mutex>
-#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -86,30 +83,13 @@ constexpr int kChains = HB_LR_CHAINS;
 constexpr int64_t kWalkBlocksPer10Sm = 36;  // level-1 log walk: 3.6 blocks of 128 threads per SM
 
 // The level-1 walk's two hot global counters (sublist claims, log-chunk
-// claims) live in one cached 2 MB block per (device, stream), 256 bytes
-// apart.  Where they land relative to each other decides how fast the walk
-// runs — in one 128-byte line 24.4 ms per 2^28-node call, 256 B or 64 KB
-// apart 15.4-15.6 ms, 4 KB apart 18.6 ms (L2 atomic-unit sharing;
-// profiles/micro_lr_chains_r02.txt) — and two separate pool allocations
-// land wherever the pool's history puts them.
-constexpr size_t kCtrJobs = 0, kCtrChunks = 256 / 8;  // u64 slots
-int walk_counters(cudaStream_t s, unsigned long long** out) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> table;
-  int dev = 0;
-  HB_CUDA_TRY(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = table.find({dev, s});
-  if (it != table.end()) {
-    *out = it->second;
-    return HB_OK;
-  }
-  unsigned long long* p = nullptr;
-  HB_CUDA_TRY(cudaMalloc(&p, (size_t)2 << 20));  // 2 MB: one large page, both counters inside it
-  table[{dev, s}] = p;
-  *out = p;
-  return HB_OK;
-}
+// claims) sit 256 bytes apart in one small stream-ordered allocation.  How
+// fast the walk runs depended on where they landed — in one 128-byte line
+// 24.4 ms per 2^28-node call, 256 B or 64 KB apart 15.4-15.6 ms, 4 KB apart
+// 18.6 ms, and 14.9-17.3 ms as the pair moved through one 2 MB page — until
+// log chunks were claimed in pairs (kChunkClaim): 14.9-15.1 ms wherever
+// they land (profiles/micro_lr_chains_r02.txt).
+constexpr size_t kCtrJobs = 0, kCtrChunks = 256 / 8, kCtrBytes = 512;  // u64 slots, bytes
 
 // Successor reads are random: load them L2-only (.cg).  The read-only
 // (.nc / __ldg) path promotes every L1 miss to a full 128-byte line, i.e.
@@ -488,22 +468,19 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     int64_t blocks = ceil_div(L->nsub, 128 * kChains);
     if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;  // 2048 resident threads / SM
     DevBuf jobs;  // dynamic sublist claiming (+1 % over a static stride: 12.62 vs 12.49 Gnodes/s)
-    HB_TRY(alloc(&jobs, 8, s));
-    HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, 8, s));
+    HB_TRY(alloc(&jobs, kCtrBytes, s));  // [kCtrJobs] sublist claims, [kCtrChunks] log-chunk claims
+    HB_CUDA_TRY(cudaMemsetAsync(jobs.ptr, 0, kCtrBytes, s));
     if (L->logged) {
       // Fewer walks in flight than the SMs could hold: 3.6 blocks of 128
       // per SM (~68K walks) from 2^27 nodes up — 14.9 vs 16.9 ms per
       // 2^28-node call and 29.5 vs 33.3 ms at 2^29 against one walk per
-      // resident thread; 4 blocks/SM is as fast in some processes (14.5) and
-      // 16.6 ms in others, 3.6 was 14.9-15.0 in every process measured — and
+      // resident thread; 4 blocks/SM is faster in some processes (14.6) and
+      // 16.8-17.2 ms in others, 3.6 was 14.9-15.1 in every process measured — and
       // 6 blocks/SM below 2^27 (3.67 vs 4.06 ms at 2^26, 1.42 vs 1.54 at
       // 2^24; neutral at 2^20-2^22).  profiles/micro_lr_chains_r02.txt.
       blocks = std::min<int64_t>(blocks, cur_n >= ((int64_t)1 << 27) ? (int64_t)di.sms * kWalkBlocksPer10Sm / 10
                                                                       : (int64_t)di.sms * 6);
-      unsigned long long* ctr = nullptr;
-      HB_TRY(walk_counters(s, &ctr));
-      HB_CUDA_TRY(cudaMemsetAsync(ctr + kCtrJobs, 0, 8, s));
-      HB_CUDA_TRY(cudaMemsetAsync(ctr + kCtrChunks, 0, 8, s));
+      unsigned long long* ctr = jobs.as<unsigned long long>();
       lr_walk_log_kernel<S><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, cur_n, cur_head, L->nsub, L->extra, L->log.as<uint64_t>(),
           ctr + kCtrChunks, L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),

@@ -827,9 +827,9 @@ class LrBench(Bench):
     def bytes_per_launch(self):
         return 12 * self.n // self.world
 
-    # log 8 + packed pairs 16 + node sort ~66 (4 passes x 16 over ~1.03 n entries; the digit
-    # histogram is counted by the pairs kernel and the int64 widen is the last pass's store)
-    SEQ_BYTES_PER_NODE = 90
+    # log ~8.3 + packed pairs ~16.5 + node sort: 2 digit passes x 16 over ~1.03 n entries (the digit
+    # histograms are counted by the pairs kernel) + the bucket finish 16 (8 read + 8 int64 rank written)
+    SEQ_BYTES_PER_NODE = 74
 
     def roofline_extra(self, ms):
         # t >= one dependent random successor read per node at the measured

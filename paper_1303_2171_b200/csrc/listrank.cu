@@ -29,8 +29,8 @@
 #include "common.cuh"
 
 namespace hb {
-int sort_pairs_widen_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int64_t n_out, int64_t* out,
-                         cudaStream_t s);
+int sort_pairs_bits_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes, DevBuf* alt,
+                        uint64_t** sorted, cudaStream_t s);
 namespace {
 
 #ifndef HB_LR_K
@@ -177,9 +177,12 @@ __global__ void __launch_bounds__(128)
 // The log walk instead appends (node, offset) to per-thread 32-entry chunks
 // of a sequential log (chunk ids from one counter; each chunk opens with a
 // marker holding its sublist id, and every walk start writes a marker).
-// After the sublist chain is ranked, the log becomes (node, rank) pairs
-// (lr_log_pairs_kernel), which the library's radix sort orders by node —
-// coalesced passes — and the ranks are widened into rank[] in node order.
+// After the sublist chain is ranked, the log becomes packed (rank, node)
+// pairs (lr_log_pack_kernel), which the library's radix sort orders by the
+// node bits above 2^13-node buckets — coalesced passes — and
+// lr_bucket_finish_kernel writes each bucket's ranks into rank[] through
+// shared memory.  (Without the atomics ranking: lr_log_pairs_kernel, a full
+// key sort and lr_widen_kernel.)
 constexpr int kLogChunk = 32;
 constexpr int kChunkClaim = 2;  // log chunks per counter claim
 constexpr uint32_t kMarkBit = 0x80000000u;
@@ -310,7 +313,8 @@ __global__ void lr_log_pairs_kernel(const uint64_t* __restrict__ log, int64_t sl
 // on the way (so the sort needs no histogram pass of its own).
 __global__ void __launch_bounds__(256) lr_log_pack_kernel(const uint64_t* __restrict__ log, int64_t slots,
                                                           const int64_t* __restrict__ prefix,
-                                                          uint64_t* __restrict__ pairs, uint32_t* __restrict__ hist) {
+                                                          uint64_t* __restrict__ pairs, uint32_t* __restrict__ hist,
+                                                          int hshift) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -330,13 +334,59 @@ __global__ void __launch_bounds__(256) lr_log_pack_kernel(const uint64_t* __rest
       const uint32_t val = node ? (uint32_t)(prefix[j] + (int64_t)(uint32_t)e) : 0u;
       __stcs(reinterpret_cast<unsigned long long*>(pairs) + i, ((unsigned long long)val << 32) | key);
 #pragma unroll
-      for (int d = 0; d < 4; ++d) atomicAdd(&h[d][(key >> (8 * d)) & 255u], 1u);
+      for (int d = 0; d < 4; ++d) atomicAdd(&h[d][(uint32_t)((uint64_t)key >> (hshift + 8 * d)) & 255u], 1u);
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
     const uint32_t c = (&h[0][0])[i];
     if (c) atomicAdd(hist + i, c);
+  }
+}
+
+// The node sort's finish.  The pairs are ordered by the node bits above BB
+// (and the markers / padding, key 0xffffffff, behind every node), and a
+// valid list has exactly one pair per node, so positions [b * 2^BB,
+// (b + 1) * 2^BB) hold exactly the nodes of bucket b: one CTA per bucket
+// places their ranks in shared memory by the low node bits and writes the
+// bucket's slice of rank[] coalesced.  This replaces the LSD passes over the
+// low bits (a random 8-byte store to rank[] would cost a DRAM sector
+// read-modify-write, micro_scatter_window_r02.txt).  BB = 13 (64 KB of
+// shared memory per CTA), 14 where that saves a digit pass (2^29 nodes).
+constexpr int kBucketThreads = 512;
+template <int BB>
+__global__ void __launch_bounds__(kBucketThreads) lr_bucket_finish_kernel(const uint64_t* __restrict__ pairs, int64_t n,
+                                                                          int64_t* __restrict__ rank,
+                                                                          unsigned long long* __restrict__ err) {
+  extern __shared__ __align__(16) int64_t s_rank[];
+  constexpr int S = 1 << BB;
+  const int64_t lo = (int64_t)blockIdx.x * S;
+  const int cnt = (int)min((int64_t)S, n - lo);
+  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(pairs + lo);
+  bool bad = false;
+  // 16-byte loads (lo is a multiple of 8192 pairs); a ragged last bucket's odd tail pair alone
+  for (int i = threadIdx.x; 2 * i < cnt; i += kBucketThreads) {
+    ulonglong2 two;
+    if (2 * i + 1 < cnt) {
+      two = __ldcs(src + i);
+    } else {
+      two.x = __ldcs(reinterpret_cast<const unsigned long long*>(pairs) + lo + 2 * i);
+      two.y = ~0ull;
+    }
+    const uint32_t k0 = (uint32_t)two.x, k1 = (uint32_t)two.y;
+    if ((int64_t)(k0 >> BB) != (int64_t)blockIdx.x) bad = true;
+    else s_rank[k0 & (S - 1)] = (int64_t)(two.x >> 32);
+    if (2 * i + 1 < cnt) {
+      if ((int64_t)(k1 >> BB) != (int64_t)blockIdx.x) bad = true;
+      else s_rank[k1 & (S - 1)] = (int64_t)(two.y >> 32);
+    }
+  }
+  if (bad) atomicAdd(err, 1ull);
+  __syncthreads();
+  longlong2* dst = reinterpret_cast<longlong2*>(rank + lo);
+  for (int i = threadIdx.x; 2 * i < cnt; i += kBucketThreads) {
+    if (2 * i + 1 < cnt) __stcs(dst + i, make_longlong2(s_rank[2 * i], s_rank[2 * i + 1]));
+    else rank[lo + 2 * i] = s_rank[2 * i];
   }
 }
 
@@ -577,16 +627,44 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       DevBuf& val = L->val;
       int64_t pb = ceil_div(slots, 256);
       if (pb > (int64_t)di.sms * 16) pb = (int64_t)di.sms * 16;
-      {  // packed pairs + digit histograms, one sort with the widen fused into its last pass
+      {  // packed pairs + digit histograms, a sort over the node bits above the buckets, the bucket finish
+        // node bits nb (nodes < 2^nb); sorted bits [b0, nb + 1): bit nb puts the markers behind every node
+        int nb = 1;
+        while (((int64_t)1 << nb) < L->n) ++nb;
+        int bb = 13;
+        int passes = std::max(1, (nb + 1 - bb + 7) / 8);
+        if (passes > 1 && (nb + 1 - 14 + 7) / 8 < passes) {
+          bb = 14;
+          --passes;
+        }
+        const int b0 = nb + 1 - 8 * passes;
         DevBuf hist;
         HB_TRY(alloc(&hist, 4 * 256 * 4, s));
         HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, 4 * 256 * 4, s));
         // the packed pairs live in `key` (8 bytes per slot)
         lr_log_pack_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, L->key.as<uint64_t>(),
-                                                   hist.as<uint32_t>());
+                                                   hist.as<uint32_t>(), b0);
         HB_TRY(check_launch());
-        const int rc = sort_pairs_widen_ext(L->key.as<uint64_t>(), slots, hist.as<uint32_t>(), L->n, dst, s);
+        DevBuf alt;
+        uint64_t* sorted = nullptr;
+        const int rc = b0 >= 0 ? sort_pairs_bits_ext(L->key.as<uint64_t>(), slots, hist.as<uint32_t>(), b0, passes,
+                                                     &alt, &sorted, s)
+                               : HB_ENOSYS;
         if (rc == HB_OK) {
+          const size_t smem = sizeof(int64_t) << bb;
+          auto k = bb == 14 ? lr_bucket_finish_kernel<14> : lr_bucket_finish_kernel<13>;
+          HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          HB_CUDA_TRY(cudaMemsetAsync(err.ptr, 0, 8, s));
+          k<<<(unsigned)ceil_div(L->n, (int64_t)1 << bb), kBucketThreads, smem, s>>>(sorted, L->n, dst,
+                                                                                     err.as<unsigned long long>());
+          HB_TRY(check_launch());
+          unsigned long long bad = 0;
+          HB_CUDA_TRY(cudaMemcpyAsync(&bad, err.ptr, 8, cudaMemcpyDeviceToHost, s));
+          HB_CUDA_TRY(cudaStreamSynchronize(s));
+          if (bad) {
+            set_error("node sort: %llu bucket(s) hold a foreign node (internal error)", bad);
+            return HB_ECUDA;
+          }
           prefix = dst;
           continue;
         }

@@ -512,7 +512,8 @@ __global__ void __launch_bounds__(T, MINB)
     onesweep_rfk_kernel(const void* __restrict__ kin_, void* __restrict__ kout_, const uint32_t* __restrict__ vin,
                         uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t flip,
                        const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
-                       uint32_t* __restrict__ tile_counter, int64_t n_out) {
+                       uint32_t* __restrict__ tile_counter) {
+  static_assert(OUTM == 0 || OUTM == 1, "output split (0) or packed (1)");
   constexpr bool POUT = OUTM == 1;
   constexpr int W = T / 32, TILE = T * I;
   static_assert(T >= 256, "one look-back thread per digit");
@@ -619,9 +620,7 @@ __global__ void __launch_bounds__(T, MINB)
   for (int j = tid; j < valid; j += T) {
     const uint64_t e = s_el[j];
     const uint32_t dst = s_goff[dig(e)] + (uint32_t)j;
-    if (OUTM == 2) {  // widen: the payload as int64 at its sorted position (positions < n_out only)
-      if ((int64_t)dst < n_out) reinterpret_cast<int64_t*>(vout)[dst] = (int64_t)(e >> 32);
-    } else if (POUT) {
+    if (POUT) {
       eout[dst] = e;
     } else {
       kout[dst] = (uint32_t)e;
@@ -704,12 +703,12 @@ bool use_atomics_rank(int flags) {
 constexpr int kPkI = 22, kPkT = 256, kPkLbw = 2, kPkMinB = 3;
 
 template <bool PIN, int OUTM>
-int launch_rfk(const PassArgs& a, cudaStream_t s, int64_t tiles, int64_t n_out = 0) {
+int launch_rfk(const PassArgs& a, cudaStream_t s, int64_t tiles) {
   const size_t smem = (size_t)kPkT * kPkI * 8;
   auto k = onesweep_rfk_kernel<PIN, OUTM, kPkI, kPkT, kPkLbw, kPkMinB>;
   HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<(unsigned)tiles, kPkT, smem, s>>>(a.kin, a.kout, a.vin, a.vout, a.n, a.shift, (uint32_t)a.flip, a.gstart,
-                                        a.lookback, a.counter, n_out);
+                                        a.lookback, a.counter);
   return check_launch();
 }
 
@@ -779,49 +778,49 @@ int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, cons
   return HB_OK;
 }
 
-// Sort packed (payload << 32 | key) pairs by key in place of a later widen:
-// all four 8-bit digit passes (PIN = packed from the first), the last one
-// writing the payload as int64 at its sorted position when that is < n_out
-// (list ranking's node sort: the first n positions hold keys 0..n-1, the
-// sentinel keys sort behind them).  hist = the four digit histograms of the
-// keys, already counted by the producer of `pairs`.  Needs the atomics
-// ranking (stable); returns HB_ENOSYS when it is not in use so the caller
-// takes the general path.
-int sort_pairs_widen(uint64_t* pairs, int64_t n, const uint32_t* hist, int64_t n_out, int64_t* out,
-                     cudaStream_t s) {
+// Order packed (payload << 32 | key) pairs by the key bits [shift0,
+// shift0 + 8 * passes): `passes` packed digit passes (PIN and POUT packed),
+// hist = their digit histograms (row p for the digit at shift0 + 8p),
+// already counted by the producer of `pairs`.  The result lands in `pairs`
+// or in *alt (allocated here, n pairs); *sorted says which.  Needs the
+// atomics ranking (stable); returns HB_ENOSYS when it is not in use so the
+// caller takes the general path.
+int sort_pairs_bits(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes, DevBuf* alt,
+                    uint64_t** sorted, cudaStream_t s) {
   if (!use_atomics_rank(0)) return HB_ENOSYS;
   if (n >= (int64_t)kCountMask) {
     set_error("radix sort supports n < 2^30 keys per call (got %lld)", (long long)n);
     return HB_EINVAL;
   }
+  if (passes < 1 || passes > 4 || shift0 < 0 || shift0 + 8 * passes > 32) return HB_EINVAL;
   const int64_t tiles = ceil_div(n, (int64_t)kPkT * kPkI);
   const size_t lb_words = (size_t)tiles * 256 + 32;
-  DevBuf gst, lb, alt;
-  HB_TRY(alloc(&gst, 4 * 256 * 4, s));
-  scan_hist_kernel<<<4, 256, 0, s>>>(hist, gst.as<uint32_t>(), 4);
+  DevBuf gst, lb;
+  HB_TRY(alloc(&gst, (size_t)passes * 256 * 4, s));
+  scan_hist_kernel<<<passes, 256, 0, s>>>(hist, gst.as<uint32_t>(), passes);
   HB_TRY(check_launch());
   HB_TRY(alloc(&lb, lb_words * 4, s));
-  HB_TRY(alloc(&alt, (size_t)n * 8, s));
+  HB_TRY(alloc(alt, (size_t)n * 8, s));
   PassArgs pa{};
   pa.n = n;
   pa.flip = 0;
   pa.lookback = lb.as<uint32_t>();
   pa.counter = lb.as<uint32_t>() + (size_t)tiles * 256;
   void* cur = pairs;
-  void* nxt = alt.ptr;
-  for (int p = 0; p < 4; ++p) {
+  void* nxt = alt->ptr;
+  for (int p = 0; p < passes; ++p) {
     HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
     pa.kin = cur;
     pa.kout = nxt;
     pa.vin = nullptr;
-    pa.vout = p == 3 ? reinterpret_cast<uint32_t*>(out) : nullptr;
-    pa.shift = 8 * p;
+    pa.vout = nullptr;
+    pa.shift = shift0 + 8 * p;
     pa.hist = hist + p * 256;
     pa.gstart = gst.as<uint32_t>() + p * 256;
-    if (p == 3) HB_TRY((launch_rfk<true, 2>(pa, s, tiles, n_out)));
-    else HB_TRY((launch_rfk<true, 1>(pa, s, tiles)));
+    HB_TRY((launch_rfk<true, 1>(pa, s, tiles)));
     std::swap(cur, nxt);
   }
+  *sorted = static_cast<uint64_t*>(cur);
   return HB_OK;
 }
 
@@ -994,9 +993,9 @@ __global__ void sort_bounds_kernel(const K* __restrict__ keys, const uint32_t* _
 }  // namespace
 
 // list ranking's node sort (csrc/listrank.cu)
-int sort_pairs_widen_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int64_t n_out, int64_t* out,
-                         cudaStream_t s) {
-  return sort_pairs_widen(pairs, n, hist, n_out, out, s);
+int sort_pairs_bits_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes, DevBuf* alt,
+                        uint64_t** sorted, cudaStream_t s) {
+  return sort_pairs_bits(pairs, n, hist, shift0, passes, alt, sorted, s);
 }
 }  // namespace hb
 

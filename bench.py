@@ -827,9 +827,9 @@ class LrBench(Bench):
     def bytes_per_launch(self):
         return 12 * self.n // self.world
 
-    # log ~8.3 + packed pairs ~16.5 + node sort: 2 digit passes x 16 over ~1.03 n entries (the digit
-    # histograms are counted by the pairs kernel) + the bucket finish 16 (8 read + 8 int64 rank written)
-    SEQ_BYTES_PER_NODE = 74
+    # log ~8.3 + node sort: 2 digit passes x 16 over ~1.03 n log slots (the walk counts the digit
+    # histograms; the first pass reads the log itself) + the bucket finish 16 (8 read + 8 int64 rank)
+    SEQ_BYTES_PER_NODE = 58
 
     def roofline_extra(self, ms):
         # t >= one dependent random successor read per node at the measured

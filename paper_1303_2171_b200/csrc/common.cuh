@@ -172,4 +172,26 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// List ranking's level-1 log (csrc/listrank.cu): 8-byte slots in 32-slot,
+// 256-byte-aligned chunks.  Node entry = node << 32 | offset in its sublist;
+// marker = (kLogMark | sublist) << 32 (every chunk opens with one, every walk
+// start inside a chunk writes one); padding = kLogEmpty << 32.
+constexpr uint32_t kLogMark = 0x80000000u;
+constexpr uint32_t kLogEmpty = 0xffffffffu;
+constexpr int kLogChunkSlots = 32;
+// One warp holds one chunk, lane = slot (all 32 lanes call this): the slot
+// as a packed (rank << 32 | node) pair, rank = prefix[sublist] + offset;
+// markers and padding become key 0xffffffff, rank 0.
+__device__ __forceinline__ uint64_t log_slot_pair(uint64_t e, const int64_t* __restrict__ prefix) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t le = (2u << lane) - 1u;  // lanes <= me
+  const uint32_t hi = (uint32_t)(e >> 32);
+  const bool mark = (hi & kLogMark) && hi != kLogEmpty;
+  const uint32_t mb = __ballot_sync(0xffffffffu, mark);
+  const int src = 31 - __clz(mb & le);
+  const uint32_t j = __shfl_sync(0xffffffffu, hi & ~kLogMark, src < 0 ? 0 : src);
+  if (hi & kLogMark) return 0xffffffffull;
+  return ((uint64_t)(uint32_t)(prefix[j] + (int64_t)(uint32_t)e) << 32) | hi;
+}
+
 }  // namespace hb

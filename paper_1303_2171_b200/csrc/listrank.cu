@@ -29,8 +29,8 @@
 #include "common.cuh"
 
 namespace hb {
-int sort_pairs_bits_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes, DevBuf* alt,
-                        uint64_t** sorted, cudaStream_t s);
+int sort_pairs_bits_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes,
+                        const int64_t* log_prefix, uint64_t* alt, uint64_t** sorted, cudaStream_t s);
 namespace {
 
 #ifndef HB_LR_K
@@ -177,16 +177,17 @@ __global__ void __launch_bounds__(128)
 // The log walk instead appends (node, offset) to per-thread 32-entry chunks
 // of a sequential log (chunk ids from one counter; each chunk opens with a
 // marker holding its sublist id, and every walk start writes a marker).
-// After the sublist chain is ranked, the log becomes packed (rank, node)
-// pairs (lr_log_pack_kernel), which the library's radix sort orders by the
-// node bits above 2^13-node buckets — coalesced passes — and
+// The walk also counts the node sort's digit histograms.  After the sublist
+// chain is ranked, the library's radix sort orders the log by the node bits
+// above 2^13-node buckets — coalesced passes, the first reading each log
+// slot as its packed (rank, node) pair (log_slot_pair) — and
 // lr_bucket_finish_kernel writes each bucket's ranks into rank[] through
 // shared memory.  (Without the atomics ranking: lr_log_pairs_kernel, a full
 // key sort and lr_widen_kernel.)
-constexpr int kLogChunk = 32;
+constexpr int kLogChunk = kLogChunkSlots;  // the log format: common.cuh
 constexpr int kChunkClaim = 2;  // log chunks per counter claim
-constexpr uint32_t kMarkBit = 0x80000000u;
-constexpr uint32_t kEmptyHi = 0xffffffffu;
+constexpr uint32_t kMarkBit = kLogMark;
+constexpr uint32_t kEmptyHi = kLogEmpty;
 constexpr int64_t kLogMin = 1 << 20;  // smaller lists: the plain walk (everything fits in L2)
 
 template <typename S>
@@ -194,18 +195,29 @@ __global__ void __launch_bounds__(128)
     lr_walk_log_kernel(const S* __restrict__ succ, int64_t n, int64_t head, int64_t nsub, int64_t extra,
                        uint64_t* __restrict__ log, unsigned long long* __restrict__ chunk_ctr, int64_t max_chunks,
                        int64_t* __restrict__ nxt, int64_t* __restrict__ len, unsigned long long* __restrict__ err,
-                       unsigned long long* __restrict__ jobs) {
+                       unsigned long long* __restrict__ jobs, uint32_t* __restrict__ hist, int hshift, int hpasses) {
   // Entries are held back in registers and stored 4 at a time (one full
   // 32-byte sector as two 16-byte stores issued together): a sector filled
   // entry by entry over microseconds would be evicted part-written and cost
   // a DRAM read-modify-write (no write mask on HBM3e).  Chunks are 256-byte
   // aligned, so every group of 4 slots is one sector.
+  // the node sort's digit histograms (digits at hshift + 8d, d < hpasses) of
+  // every slot written, so the sort needs no counting pass over the log
+  __shared__ uint32_t hcount[2][256];
+  for (int i = threadIdx.x; i < 2 * 256; i += blockDim.x) (&hcount[0][0])[i] = 0;
+  __syncthreads();
+  auto count = [&](uint32_t hi, uint32_t times) {
+    const uint32_t key = (hi & kMarkBit) ? 0xffffffffu : hi;
+    atomicAdd(&hcount[0][(key >> hshift) & 255u], times);
+    if (hpasses > 1) atomicAdd(&hcount[1][(key >> (hshift + 8)) & 255u], times);
+  };
   int64_t cbase = 0;
   int fill = kLogChunk;  // no chunk yet
   bool overflow = false;
   uint64_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
   int nb = 0;
   auto push = [&](uint64_t e) {  // next slot of the current chunk
+    count((uint32_t)(e >> 32), 1u);
     if (nb == 0) b0 = e;
     else if (nb == 1) b1 = e;
     else if (nb == 2) b2 = e;
@@ -281,7 +293,13 @@ __global__ void __launch_bounds__(128)
       ulonglong2* p = reinterpret_cast<ulonglong2*>(log + spare * kLogChunk);
 #pragma unroll
       for (int k = 0; k < kLogChunk / 2; ++k) __stcs(p + k, pad);
+      count(kEmptyHi, kLogChunk);
     }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hpasses * 256; i += blockDim.x) {
+    const uint32_t c = (&hcount[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
   }
 }
 
@@ -305,42 +323,6 @@ __global__ void lr_log_pairs_kernel(const uint64_t* __restrict__ log, int64_t sl
       key[i] = node ? hi : 0xffffffffu;
       val[i] = node ? (uint32_t)(prefix[j] + (int64_t)(uint32_t)e) : 0u;
     }
-  }
-}
-
-// The same conversion written as packed (val << 32 | key) elements for the
-// library's pair sort, counting the four 8-bit digit histograms of the keys
-// on the way (so the sort needs no histogram pass of its own).
-__global__ void __launch_bounds__(256) lr_log_pack_kernel(const uint64_t* __restrict__ log, int64_t slots,
-                                                          const int64_t* __restrict__ prefix,
-                                                          uint64_t* __restrict__ pairs, uint32_t* __restrict__ hist,
-                                                          int hshift) {
-  __shared__ uint32_t h[4][256];
-  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint32_t le = (2u << lane) - 1u;  // lanes <= me
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < slots;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = i < slots ? __ldcs(reinterpret_cast<const unsigned long long*>(log) + i) : ((uint64_t)kEmptyHi << 32);
-    const uint32_t hi = (uint32_t)(e >> 32);
-    const bool mark = (hi & kMarkBit) && hi != kEmptyHi;
-    const uint32_t mb = __ballot_sync(0xffffffffu, mark);
-    const int src = 31 - __clz(mb & le);
-    const uint32_t j = __shfl_sync(0xffffffffu, hi & ~kMarkBit, src < 0 ? 0 : src);
-    if (i < slots) {
-      const bool node = !(hi & kMarkBit);
-      const uint32_t key = node ? hi : 0xffffffffu;
-      const uint32_t val = node ? (uint32_t)(prefix[j] + (int64_t)(uint32_t)e) : 0u;
-      __stcs(reinterpret_cast<unsigned long long*>(pairs) + i, ((unsigned long long)val << 32) | key);
-#pragma unroll
-      for (int d = 0; d < 4; ++d) atomicAdd(&h[d][(uint32_t)((uint64_t)key >> (hshift + 8 * d)) & 255u], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
-    const uint32_t c = (&h[0][0])[i];
-    if (c) atomicAdd(hist + i, c);
   }
 }
 
@@ -459,8 +441,9 @@ struct Level {
   int64_t n = 0, nsub = 0, extra = -1, head = 0;
   // level 0 with the log walk
   bool logged = false;
-  DevBuf log, ctr, key, val;
+  DevBuf log, ctr, key, hist;
   int64_t max_chunks = 0;
+  int sort_shift = 0, sort_passes = 0, bucket_bits = 0;  // the node sort (bucket finish)
 };
 
 // Rank the list `succ` (n nodes, first node `head`): out_rank[v] = sum of the
@@ -500,13 +483,27 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     if (L->logged) {
       // every full chunk holds >= 31 node / walk-start entries; plus one partial chunk per thread
       L->max_chunks = (cur_n + L->nsub) / (kLogChunk - 1) + (int64_t)di.sms * 16 * 128 * kChunkClaim + 64;
-      // log + (node, rank) pair arrays allocated together, up front: the same
+      // log + the sort's second buffer allocated together, up front: the same
       // allocation pattern every call keeps the stream-ordered pool from growing
       HB_TRY(alloc(&L->log, (size_t)L->max_chunks * kLogChunk * 8, s));
-      HB_TRY(alloc(&L->key, (size_t)L->max_chunks * kLogChunk * 8, s));  // packed (rank, node) pairs
-      HB_TRY(alloc(&L->val, (size_t)L->max_chunks * kLogChunk * 4, s));
+      HB_TRY(alloc(&L->key, (size_t)L->max_chunks * kLogChunk * 8, s));
       HB_TRY(alloc(&L->ctr, 8, s));
       HB_CUDA_TRY(cudaMemsetAsync(L->ctr.ptr, 0, 8, s));
+      // The node sort orders the (rank, node) pairs by the node bits above a
+      // 2^bucket_bits-node bucket (2^13; 2^14 where that saves a pass) and up
+      // to bit nb, nodes < 2^nb: markers and padding (key 0xffffffff) have
+      // bit nb set and sort behind every node.
+      int nb = 1;
+      while (((int64_t)1 << nb) < cur_n) ++nb;
+      L->bucket_bits = 13;
+      L->sort_passes = std::max(1, (nb + 1 - 13 + 7) / 8);
+      if (L->sort_passes > 1 && (nb + 1 - 14 + 7) / 8 < L->sort_passes) {
+        L->bucket_bits = 14;
+        --L->sort_passes;
+      }
+      L->sort_shift = nb + 1 - 8 * L->sort_passes;
+      HB_TRY(alloc(&L->hist, 2 * 256 * 4, s));
+      HB_CUDA_TRY(cudaMemsetAsync(L->hist.ptr, 0, 2 * 256 * 4, s));
     } else if (first) {
       L->tmp.ptr = out_rank;  // packed (sublist, offset) lives in the output until expanded
       L->tmp.owned = false;
@@ -534,7 +531,7 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       lr_walk_log_kernel<S><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, cur_n, cur_head, L->nsub, L->extra, L->log.as<uint64_t>(),
           ctr + kCtrChunks, L->max_chunks, L->nxt.as<int64_t>(), L->len.as<int64_t>(),
-          err.as<unsigned long long>(), ctr + kCtrJobs);
+          err.as<unsigned long long>(), ctr + kCtrJobs, L->hist.as<uint32_t>(), L->sort_shift, L->sort_passes);
       // the chunk count the pairs pass reads back
       HB_CUDA_TRY(cudaMemcpyAsync(L->ctr.ptr, ctr + kCtrChunks, 8, cudaMemcpyDeviceToDevice, s));
     } else if (first && w0 != nullptr) {
@@ -623,34 +620,12 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
       HB_CUDA_TRY(cudaMemcpyAsync(&used, L->ctr.ptr, 8, cudaMemcpyDeviceToHost, s));
       HB_CUDA_TRY(cudaStreamSynchronize(s));
       const int64_t slots = (int64_t)std::min<unsigned long long>(used, (unsigned long long)L->max_chunks) * kLogChunk;
-      DevBuf& key = L->key;
-      DevBuf& val = L->val;
-      int64_t pb = ceil_div(slots, 256);
-      if (pb > (int64_t)di.sms * 16) pb = (int64_t)di.sms * 16;
-      {  // packed pairs + digit histograms, a sort over the node bits above the buckets, the bucket finish
-        // node bits nb (nodes < 2^nb); sorted bits [b0, nb + 1): bit nb puts the markers behind every node
-        int nb = 1;
-        while (((int64_t)1 << nb) < L->n) ++nb;
-        int bb = 13;
-        int passes = std::max(1, (nb + 1 - bb + 7) / 8);
-        if (passes > 1 && (nb + 1 - 14 + 7) / 8 < passes) {
-          bb = 14;
-          --passes;
-        }
-        const int b0 = nb + 1 - 8 * passes;
-        DevBuf hist;
-        HB_TRY(alloc(&hist, 4 * 256 * 4, s));
-        HB_CUDA_TRY(cudaMemsetAsync(hist.ptr, 0, 4 * 256 * 4, s));
-        // the packed pairs live in `key` (8 bytes per slot)
-        lr_log_pack_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, L->key.as<uint64_t>(),
-                                                   hist.as<uint32_t>(), b0);
-        HB_TRY(check_launch());
-        DevBuf alt;
+      {  // the node sort over the bits above the buckets — its first pass reads the log — and the bucket finish
         uint64_t* sorted = nullptr;
-        const int rc = b0 >= 0 ? sort_pairs_bits_ext(L->key.as<uint64_t>(), slots, hist.as<uint32_t>(), b0, passes,
-                                                     &alt, &sorted, s)
-                               : HB_ENOSYS;
+        const int rc = sort_pairs_bits_ext(L->log.as<uint64_t>(), slots, L->hist.as<uint32_t>(), L->sort_shift,
+                                           L->sort_passes, prefix, L->key.as<uint64_t>(), &sorted, s);
         if (rc == HB_OK) {
+          const int bb = L->bucket_bits;
           const size_t smem = sizeof(int64_t) << bb;
           auto k = bb == 14 ? lr_bucket_finish_kernel<14> : lr_bucket_finish_kernel<13>;
           HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -670,17 +645,19 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
         }
         if (rc != HB_ENOSYS) return rc;
       }
+      int64_t pb = ceil_div(slots, 256);
+      if (pb > (int64_t)di.sms * 16) pb = (int64_t)di.sms * 16;
+      uint32_t* key = L->key.as<uint32_t>();  // (node, rank) as two u32 arrays in the sort buffer
+      uint32_t* val = key + slots;
       // general path (ballot-ranked sorts): (node, rank) as two arrays, sort, widen
-      lr_log_pairs_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, key.as<uint32_t>(),
-                                                 val.as<uint32_t>());
+      lr_log_pairs_kernel<<<(int)pb, 256, 0, s>>>(L->log.as<uint64_t>(), slots, prefix, key, val);
       HB_TRY(check_launch());
       // order the pairs by node: the first n keys are 0..n-1 (a valid list has
       // one log entry per node; the chain check above guarantees it)
-      HB_TRY(hb_sort(key.ptr, key.ptr, HB_U32, val.as<uint32_t>(), val.as<uint32_t>(), slots, nullptr,
-                     HB_DEVICE_PTRS | HB_ASYNC, s));
+      HB_TRY(hb_sort(key, key, HB_U32, val, val, slots, nullptr, HB_DEVICE_PTRS | HB_ASYNC, s));
       int64_t wb = ceil_div(L->n, 256);
       if (wb > (int64_t)di.sms * 16) wb = (int64_t)di.sms * 16;
-      lr_widen_kernel<<<(int)wb, 256, 0, s>>>(val.as<uint32_t>(), L->n, dst);
+      lr_widen_kernel<<<(int)wb, 256, 0, s>>>(val, L->n, dst);
       HB_TRY(check_launch());
       prefix = dst;
       continue;

@@ -502,18 +502,21 @@ __global__ void __launch_bounds__(T, MINB)
 }
 
 // u32 keys + u32 payload moved as ONE 8-byte element (key in the low half):
-// PIN — the input is packed (else key and payload arrays), POUT — the output
-// is packed (else split back into the two arrays).  The first live digit pass
-// reads split and writes packed, the middle passes stay packed, the last one
-// writes split: one 8-byte load / smem store / smem load / global store per
-// element instead of two of each.
-template <bool PIN, int OUTM, int I, int T, int LBW, int MINB>
+// INM — the input is key and payload arrays (0), packed (1), or list
+// ranking's level-1 log (2: log_slot_pair turns each slot into its packed
+// pair on the load, prefix = the ranked sublist starts); OUTM — the output is
+// packed (1) or split back into the two arrays (0).  The first live digit
+// pass reads split and writes packed, the middle passes stay packed, the
+// last one writes split: one 8-byte load / smem store / smem load / global
+// store per element instead of two of each.
+template <int INM, int OUTM, int I, int T, int LBW, int MINB>
 __global__ void __launch_bounds__(T, MINB)
     onesweep_rfk_kernel(const void* __restrict__ kin_, void* __restrict__ kout_, const uint32_t* __restrict__ vin,
                         uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t flip,
                        const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
-                       uint32_t* __restrict__ tile_counter) {
+                       uint32_t* __restrict__ tile_counter, const int64_t* __restrict__ prefix) {
   static_assert(OUTM == 0 || OUTM == 1, "output split (0) or packed (1)");
+  static_assert(INM != 2 || (T * I) % kLogChunkSlots == 0, "log tiles are whole chunks");
   constexpr bool POUT = OUTM == 1;
   constexpr int W = T / 32, TILE = T * I;
   static_assert(T >= 256, "one look-back thread per digit");
@@ -543,7 +546,8 @@ __global__ void __launch_bounds__(T, MINB)
   for (int i = 0; i < I; ++i) {
     const int idx = wbase + i * 32 + lane;
     const bool ok = idx < valid;
-    if (PIN) el[i] = ok ? ein[base + idx] : (uint64_t)(~0u ^ flip);
+    if (INM == 2) el[i] = log_slot_pair(ok ? ein[base + idx] : (uint64_t)kLogEmpty << 32, prefix);
+    else if (INM == 1) el[i] = ok ? ein[base + idx] : (uint64_t)(~0u ^ flip);
     else el[i] = ok ? ((uint64_t)vin[base + idx] << 32) | kin[base + idx] : (uint64_t)(~0u ^ flip);
   }
   uint32_t gs = 0;
@@ -656,6 +660,7 @@ struct PassArgs {
   const void* kin; void* kout; const uint32_t* vin; uint32_t* vout;
   int64_t n; int shift; uint64_t flip; const uint32_t* hist; uint32_t* lookback; uint32_t* counter;
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
+  const int64_t* prefix;   // INM 2 (log input): ranked sublist starts
 };
 
 bool production_rank_selftest();
@@ -702,13 +707,13 @@ bool use_atomics_rank(int flags) {
 // 24: 57.4, 20: 55.6)
 constexpr int kPkI = 22, kPkT = 256, kPkLbw = 2, kPkMinB = 3;
 
-template <bool PIN, int OUTM>
+template <int INM, int OUTM>
 int launch_rfk(const PassArgs& a, cudaStream_t s, int64_t tiles) {
   const size_t smem = (size_t)kPkT * kPkI * 8;
-  auto k = onesweep_rfk_kernel<PIN, OUTM, kPkI, kPkT, kPkLbw, kPkMinB>;
+  auto k = onesweep_rfk_kernel<INM, OUTM, kPkI, kPkT, kPkLbw, kPkMinB>;
   HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<(unsigned)tiles, kPkT, smem, s>>>(a.kin, a.kout, a.vin, a.vout, a.n, a.shift, (uint32_t)a.flip, a.gstart,
-                                        a.lookback, a.counter);
+                                        a.lookback, a.counter, a.prefix);
   return check_launch();
 }
 
@@ -768,9 +773,9 @@ int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, cons
     pa.shift = 8 * p; pa.flip = (uint64_t)flip; pa.hist = hist.as<uint32_t>() + p * 256;
     pa.lookback = lb.as<uint32_t>(); pa.counter = counter; pa.gstart = gst.as<uint32_t>() + p * 256;
     if (first && last) return HB_EINVAL;  // nlive >= 2 on this path
-    if (first) HB_TRY((launch_rfk<false, 1>(pa, s, tiles)));
-    else if (last) HB_TRY((launch_rfk<true, 0>(pa, s, tiles)));
-    else HB_TRY((launch_rfk<true, 1>(pa, s, tiles)));
+    if (first) HB_TRY((launch_rfk<0, 1>(pa, s, tiles)));
+    else if (last) HB_TRY((launch_rfk<1, 0>(pa, s, tiles)));
+    else HB_TRY((launch_rfk<1, 1>(pa, s, tiles)));
     cur = nxt;
     nxt = (nxt == pA.ptr) ? pB.ptr : pA.ptr;
     ++done;
@@ -779,14 +784,16 @@ int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, cons
 }
 
 // Order packed (payload << 32 | key) pairs by the key bits [shift0,
-// shift0 + 8 * passes): `passes` packed digit passes (PIN and POUT packed),
-// hist = their digit histograms (row p for the digit at shift0 + 8p),
-// already counted by the producer of `pairs`.  The result lands in `pairs`
-// or in *alt (allocated here, n pairs); *sorted says which.  Needs the
-// atomics ranking (stable); returns HB_ENOSYS when it is not in use so the
-// caller takes the general path.
-int sort_pairs_bits(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes, DevBuf* alt,
-                    uint64_t** sorted, cudaStream_t s) {
+// shift0 + 8 * passes): `passes` packed digit passes, hist = their digit
+// histograms (row p for the digit at shift0 + 8p), already counted by the
+// producer of `pairs`.  With log_prefix, `pairs` is list ranking's level-1
+// log and the first pass reads each slot as its packed pair (INM 2).  The
+// passes ping-pong between `pairs` and `alt` (n pairs, the caller's); the
+// result lands in *sorted (one of the two).  Needs the atomics ranking
+// (stable); returns HB_ENOSYS when it is not in use so the caller takes the
+// general path.
+int sort_pairs_bits(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes,
+                    const int64_t* log_prefix, uint64_t* alt, uint64_t** sorted, cudaStream_t s) {
   if (!use_atomics_rank(0)) return HB_ENOSYS;
   if (n >= (int64_t)kCountMask) {
     set_error("radix sort supports n < 2^30 keys per call (got %lld)", (long long)n);
@@ -800,14 +807,13 @@ int sort_pairs_bits(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0
   scan_hist_kernel<<<passes, 256, 0, s>>>(hist, gst.as<uint32_t>(), passes);
   HB_TRY(check_launch());
   HB_TRY(alloc(&lb, lb_words * 4, s));
-  HB_TRY(alloc(alt, (size_t)n * 8, s));
   PassArgs pa{};
   pa.n = n;
   pa.flip = 0;
   pa.lookback = lb.as<uint32_t>();
   pa.counter = lb.as<uint32_t>() + (size_t)tiles * 256;
   void* cur = pairs;
-  void* nxt = alt->ptr;
+  void* nxt = alt;
   for (int p = 0; p < passes; ++p) {
     HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
     pa.kin = cur;
@@ -817,7 +823,9 @@ int sort_pairs_bits(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0
     pa.shift = shift0 + 8 * p;
     pa.hist = hist + p * 256;
     pa.gstart = gst.as<uint32_t>() + p * 256;
-    HB_TRY((launch_rfk<true, 1>(pa, s, tiles)));
+    pa.prefix = log_prefix;
+    if (p == 0 && log_prefix) HB_TRY((launch_rfk<2, 1>(pa, s, tiles)));
+    else HB_TRY((launch_rfk<1, 1>(pa, s, tiles)));
     std::swap(cur, nxt);
   }
   *sorted = static_cast<uint64_t*>(cur);
@@ -993,9 +1001,9 @@ __global__ void sort_bounds_kernel(const K* __restrict__ keys, const uint32_t* _
 }  // namespace
 
 // list ranking's node sort (csrc/listrank.cu)
-int sort_pairs_bits_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes, DevBuf* alt,
-                        uint64_t** sorted, cudaStream_t s) {
-  return sort_pairs_bits(pairs, n, hist, shift0, passes, alt, sorted, s);
+int sort_pairs_bits_ext(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0, int passes,
+                        const int64_t* log_prefix, uint64_t* alt, uint64_t** sorted, cudaStream_t s) {
+  return sort_pairs_bits(pairs, n, hist, shift0, passes, log_prefix, alt, sorted, s);
 }
 }  // namespace hb
 

@@ -40,16 +40,32 @@ constexpr int kK = HB_LR_K;   // sublist spacing (node index multiple)
 constexpr int kBase = 4096;   // top level size ranked in one CTA
 
 // Validation: out[0] += tails (succ == -1), out[1] += out-of-range successors.
+// 16-byte loads, four in flight per thread (a pure read stream of n * sizeof(S) bytes).
 template <typename S>
 __global__ void lr_check_kernel(const S* __restrict__ succ, int64_t n,
                                 unsigned long long* __restrict__ out) {
+  constexpr int V = 16 / sizeof(S), U = 4;  // successors per 16-byte load, loads in flight
   unsigned long long tails = 0, bad = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = (int64_t)succ[i];
+  auto test = [&](int64_t s) {
     tails += (s == -1);
     bad += (s < -1 || s >= n);
+  };
+  const int64_t nv = ((uintptr_t)succ & 15) ? 0 : n / V;  // whole 16-byte vectors (a caller's view may be unaligned)
+  const uint4* sv = reinterpret_cast<const uint4*>(succ);
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += T * U) {
+    uint4 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = i + u * T < nv ? __ldcs(sv + i + u * T) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i + u * T >= nv) continue;
+      const S* e = reinterpret_cast<const S*>(&w[u]);
+#pragma unroll
+      for (int k = 0; k < V; ++k) test((int64_t)e[k]);
+    }
   }
+  for (int64_t i = nv * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) test((int64_t)succ[i]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     tails += __shfl_xor_sync(0xffffffffu, tails, o);
@@ -61,11 +77,24 @@ __global__ void lr_check_kernel(const S* __restrict__ succ, int64_t n,
   }
 }
 
-__device__ __forceinline__ bool is_head(int64_t v, int64_t head) { return (v % kK) == 0 || v == head; }
+// Sublist heads of a level with spacing 2^ks: node indices that are
+// multiples of 2^ks, plus the list head.  Level 1 (the input list) uses
+// kK = 64 — the layout hb_lr_layout publishes; the levels above use
+// kUpperShift (shorter sublists: those walks are few, so their time is the
+// longest sublist's, ~2^ks * ln(sublists) dependent steps).
+constexpr int kKShift = 6;
+static_assert((1 << kKShift) == kK, "kK is a power of two");
+#ifndef HB_LR_UPPER_SHIFT
+#define HB_LR_UPPER_SHIFT 3  // levels >= 2 of a 2^28-node list: spacing 64 -> 536 us, 8 -> 339, 4 -> 365 (ncu, cold)
+#endif
+constexpr int kUpperShift = HB_LR_UPPER_SHIFT;
+__device__ __forceinline__ bool is_head(int64_t v, int64_t head, int ks) {
+  return (v & ((1ll << ks) - 1)) == 0 || v == head;
+}
 
-// sublist id of a head node: v/K for multiples of K, `extra` for the list head otherwise
-__device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra) {
-  return (v % kK) == 0 ? v / kK : extra;
+// sublist id of a head node: v / 2^ks for multiples of 2^ks, `extra` for the list head otherwise
+__device__ __forceinline__ int64_t sub_id(int64_t v, int64_t head, int64_t extra, int ks) {
+  return (v & ((1ll << ks) - 1)) == 0 ? v >> ks : extra;
 }
 
 // Sublist walks.  tmp[v] = (sublist << 32) | local offset; nxt[j] = next
@@ -114,7 +143,7 @@ __global__ void __launch_bounds__(128)
     lr_walk_kernel(const S* __restrict__ succ, const int64_t* __restrict__ w, int64_t n, int64_t head,
                    int64_t nsub, int64_t extra, uint64_t* __restrict__ tmp, int64_t* __restrict__ nxt,
                    int64_t* __restrict__ len, unsigned long long* __restrict__ err,
-                   unsigned long long* __restrict__ jobs) {
+                   unsigned long long* __restrict__ jobs, int ks) {
   // jobs != nullptr: sublists are claimed from a global counter as chains
   // free up (dynamic balance: a thread's walks are geometric-length, so a
   // static stride leaves stragglers); else the static stride t, t+T, ...
@@ -126,7 +155,7 @@ __global__ void __launch_bounds__(128)
       const int64_t jj = jobs ? (int64_t)atomicAdd(jobs, 1ull) : job;
       if (jj >= nsub) break;
       job += T;
-      const int64_t h = jj == extra ? head : jj * kK;
+      const int64_t h = jj == extra ? head : jj << ks;
       if (h >= n) {
         nxt[jj] = -1;
         len[jj] = 0;
@@ -150,9 +179,9 @@ __global__ void __launch_bounds__(128)
       if (j[c] < 0) continue;
       any = true;
       const int64_t v = cur[c];
-      if (v == -1 || is_head(v, head) || steps[c] > n) {
+      if (v == -1 || is_head(v, head, ks) || steps[c] > n) {
         if (steps[c] > n) atomicAdd(err, 1ull);  // cycle without a sublist head
-        nxt[j[c]] = (v == -1 || steps[c] > n) ? -1 : sub_id(v, head, extra);
+        nxt[j[c]] = (v == -1 || steps[c] > n) ? -1 : sub_id(v, head, extra, ks);
         // a runaway walk reports more weight than the whole list holds, so a
         // chain check on the summaries alone (sharded ranking) still fails
         len[j[c]] = steps[c] > n ? n + 1 : acc[c];
@@ -270,14 +299,14 @@ __global__ void __launch_bounds__(128)
     put((uint64_t)h << 32, j);
     int64_t acc = 1, steps = 0;
     int64_t v = ld_succ(succ + h);
-    while (v != -1 && !is_head(v, head) && steps <= n) {
+    while (v != -1 && !is_head(v, head, kKShift) && steps <= n) {
       put(((uint64_t)v << 32) | (uint64_t)(uint32_t)acc, j);
       ++acc;
       ++steps;
       v = ld_succ(succ + v);
     }
     if (steps > n) atomicAdd(err, 1ull);  // cycle without a sublist head
-    nxt[jj] = (v == -1 || steps > n) ? -1 : sub_id(v, head, extra);
+    nxt[jj] = (v == -1 || steps > n) ? -1 : sub_id(v, head, extra, kKShift);
     len[jj] = steps > n ? n + 1 : acc;
   };
   for (;;) {
@@ -444,6 +473,7 @@ struct Level {
   DevBuf log, ctr, key, hist;
   int64_t max_chunks = 0;
   int sort_shift = 0, sort_passes = 0, bucket_bits = 0;  // the node sort (bucket finish)
+  int ks = 0;  // sublist spacing 2^ks
 };
 
 // Rank the list `succ` (n nodes, first node `head`): out_rank[v] = sum of the
@@ -476,8 +506,10 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     levels.push_back(L);
     L->n = cur_n;
     L->head = cur_head;
-    const int64_t regular = ceil_div(cur_n, kK);
-    L->extra = (cur_head % kK == 0) ? -1 : regular;
+    const int ks = first ? kKShift : kUpperShift;  // sublist spacing 2^ks
+    L->ks = ks;
+    const int64_t regular = ceil_div(cur_n, (int64_t)1 << ks);
+    L->extra = (cur_head & (((int64_t)1 << ks) - 1)) == 0 ? -1 : regular;
     L->nsub = regular + (L->extra >= 0 ? 1 : 0);
     L->logged = first && w0 == nullptr && cur_n >= kLogMin && cur_n <= (1ll << 29);  // sort size < 2^30
     if (L->logged) {
@@ -537,20 +569,20 @@ int rank_levels(const S* succ, const int64_t* w0, int64_t n, int64_t head, int64
     } else if (first && w0 != nullptr) {
       lr_walk_kernel<S, true><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, w0, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
-          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>(), ks);
     } else if (first) {
       lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(
           (const S*)cur_succ, nullptr, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
-          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>(), ks);
     } else {
       lr_walk_kernel<int64_t, true><<<(int)blocks, 128, 0, s>>>(
           (const int64_t*)cur_succ, w, cur_n, cur_head, L->nsub, L->extra, L->tmp.as<uint64_t>(),
-          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>());
+          L->nxt.as<int64_t>(), L->len.as<int64_t>(), err.as<unsigned long long>(), jobs.as<unsigned long long>(), ks);
     }
     HB_TRY(check_launch());
     cur_succ = L->nxt.ptr;
     w = L->len.as<int64_t>();
-    cur_head = L->extra >= 0 ? L->extra : cur_head / kK;
+    cur_head = L->extra >= 0 ? L->extra : cur_head >> ks;
     cur_n = L->nsub;
     first = false;
   }
@@ -756,7 +788,7 @@ int walk_part(const S* succ, int64_t n, int64_t head, int64_t lo, int64_t hi, ui
   int64_t blocks = ceil_div(hi - lo, 128 * kChains);
   if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
   lr_walk_kernel<S, false><<<(int)blocks, 128, 0, s>>>(succ, nullptr, n, head, hi, extra, packed, nxt, len,
-                                                       err.as<unsigned long long>(), jobs.as<unsigned long long>());
+                                                       err.as<unsigned long long>(), jobs.as<unsigned long long>(), kKShift);
   HB_TRY(check_launch());
   return HB_OK;
 }

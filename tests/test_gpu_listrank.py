@@ -75,6 +75,32 @@ def test_device_resident():
     assert np.array_equal(got.cpu().numpy(), olr.chase(succ, head))
 
 
+@pytest.mark.parametrize("dtype", ["int32", "int64"])
+def test_unaligned_device_views_and_range_check(dtype):
+    """Device successors passed as views at every 4/8-byte offset inside a
+    16-byte vector (the pre-check reads aligned arrays with 16-byte loads),
+    valid and with one out-of-range successor at the start, the middle and
+    the scalar tail."""
+    import torch
+
+    tdt = getattr(torch, dtype)
+    n = 1_000_003
+    succ, head = ods.linked_list(n, 7)
+    want = olr.chase(succ, head)
+    for off in range(16 // torch.tensor([], dtype=tdt).element_size()):
+        big = torch.zeros(n + off, dtype=tdt, device="cuda")
+        view = big[off:]
+        view.copy_(torch.from_numpy(succ.astype(dtype)))
+        assert np.array_equal(gpu_list_rank(view, head).cpu().numpy(), want), off
+        for at in (0, n // 2, n - 1):
+            bad = view.clone() if off == 0 else view
+            keep = int(bad[at])
+            bad[at] = n + 5
+            with pytest.raises(StructuralError):
+                gpu_list_rank(bad, head)
+            bad[at] = keep
+
+
 def test_broken_lists_raise():
     for succ, head in ((np.array([1, 0]), 0), (np.array([-1, -1]), 0), (np.array([5]), 0), (np.array([-1]), 3)):
         with pytest.raises(StructuralError):

@@ -1147,6 +1147,7 @@ __global__ void __launch_bounds__(32 * kSellWarps, kSellMinB)
   auto stv = [&](int s) { return reinterpret_cast<const double*>(wsm + s * kSellStage); };
   auto stc = [&](int s) { return reinterpret_cast<const int32_t*>(wsm + s * kSellStage + kSellCJ * 32 * 8); };
   const uint64_t keep = l2_evict_last();
+  const uint64_t once = l2_evict_first();  // the matrix streams through once: leave L2 to x
   const int64_t t0 = row0 / 32, t1 = (row1 + 31) / 32;
   const int64_t nwarps = (int64_t)gridDim.x * kSellWarps;
   const int64_t first = t0 + (int64_t)blockIdx.x * kSellWarps + warp;
@@ -1160,8 +1161,8 @@ __global__ void __launch_bounds__(32 * kSellWarps, kSellMinB)
     const uint32_t vb = (uint32_t)nj * 256u, cb = (uint32_t)nj * 128u;
     mbar_expect_tx(&full[s], vb + cb);  // 0 bytes (empty tile) completes the phase at once
     if (nj > 0) {
-      tma_bulk_g2s(const_cast<double*>(stv(s)), sval + base + p_j * 32, vb, &full[s]);
-      tma_bulk_g2s(const_cast<int32_t*>(stc(s)), scol + base + p_j * 32, cb, &full[s]);
+      tma_bulk_g2s_hint(const_cast<double*>(stv(s)), sval + base + p_j * 32, vb, &full[s], once);
+      tma_bulk_g2s_hint(const_cast<int32_t*>(stc(s)), scol + base + p_j * 32, cb, &full[s], once);
     }
     p_j += kSellCJ;
     if (p_j >= p_len) {  // every tile has >= 1 item, so empty rows still write 0

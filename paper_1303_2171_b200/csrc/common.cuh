@@ -101,7 +101,7 @@ bool device_view(void* host, void** dev);
 // fn(0..n-1) on the process-wide host thread pool (one region at a time).
 void host_parallel(int n, const std::function<void(int)>& fn);
 // the same on a second pool reserved for the host-share (DeviceA) kernels
-void host_kernel_parallel(int n, const std::function<void(int)>& fn);
+void host_kernel_parallel(int n, const std::function<void(int)>& fn, int max_threads);
 int host_threads();
 // Host-buffer row filters: H2D of input rows (on a side stream), the kernel
 // of each row chunk on `s` (launch(a, b) = absolute rows [a, b)), D2H of the

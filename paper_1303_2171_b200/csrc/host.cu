@@ -23,14 +23,27 @@ namespace hb {
 namespace {
 
 template <typename F>
-void parallel_chunks(int64_t n, int workers, F&& fn) {
-  // contiguous chunks [k*n/w, (k+1)*n/w), one task each (the reference's
-  // split), on the persistent host-kernel pool (no thread spawn per call)
-  if (workers <= 1 || n < 2) {
-    fn(0, 0, n);
+void parallel_chunks(int64_t n, int tasks, int workers, F&& fn) {
+  // contiguous chunks [k*n/t, (k+1)*n/t), task k each, claimed dynamically by
+  // at most `workers` threads of the persistent host-kernel pool (no thread
+  // spawn per call)
+  if (tasks <= 1 || workers <= 1 || n < 2) {
+    for (int k = 0; k < std::max(1, tasks); ++k) fn(k, n * k / std::max(1, tasks), n * (k + 1) / std::max(1, tasks));
     return;
   }
-  host_kernel_parallel(workers, [&](int k) { fn(k, n * k / workers, n * (k + 1) / workers); });
+  host_kernel_parallel(tasks, [&](int k) { fn(k, n * k / tasks, n * (k + 1) / tasks); }, workers);
+}
+
+// Tasks for `workers` threads over n units: up to kOversplit per worker (the
+// pool claims them dynamically, so a thread that shares its core with another
+// busy thread — e.g. the GPU side's synchronising caller — runs fewer chunks
+// instead of holding up the whole host share with one static chunk), at
+// least `min_units` units per task.  Chunking never changes a result: every
+// host kernel's output is per element, per row or an integer sum.
+constexpr int kOversplit = 16;
+int task_count(int64_t n, int workers, int64_t min_units) {
+  const int64_t by_size = std::max<int64_t>(1, n / std::max<int64_t>(1, min_units));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)workers * kOversplit, by_size));
 }
 
 int clamp_workers(int w) {
@@ -102,7 +115,7 @@ int64_t idx_at(const void* p, int code, int64_t i) {
 template <typename IN>
 void conv_rows(const IN* img, int H, int W, int R, const double* w, int row0, int row1, double* out, int workers) {
   const int S = 2 * R + 1;
-  parallel_chunks(row1 - row0, workers, [&](int, int64_t a, int64_t b) {
+  parallel_chunks(row1 - row0, task_count(row1 - row0, workers, 1), workers, [&](int, int64_t a, int64_t b) {
     for (int64_t rr = a; rr < b; ++rr) {
       const int y = row0 + (int)rr;
       double* o = out + rr * W;
@@ -145,10 +158,13 @@ extern "C" int hb_host_hist(const void* data, int dtype, int64_t n, int32_t bin_
   HB_CHECK_ARG(bin_count >= 1, "bin_count must be >= 1");
   HB_CHECK_ARG(bins_out && (n == 0 || data), "NULL pointer");
   workers = clamp_workers(workers);
-  std::vector<std::vector<uint64_t>> priv((size_t)workers, std::vector<uint64_t>((size_t)bin_count, 0));
-  std::vector<char> ok((size_t)workers, 1);
+  // one private table per task: >= 2^18-element tasks, tables capped at 64 MB
+  const int tasks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(task_count(n, workers, 1 << 18), (64ll << 20) / (8ll * bin_count)));
+  std::vector<std::vector<uint64_t>> priv((size_t)tasks, std::vector<uint64_t>((size_t)bin_count, 0));
+  std::vector<char> ok((size_t)tasks, 1);
   bool supported = true;
-  parallel_chunks(n, workers, [&](int k, int64_t a, int64_t b) {
+  parallel_chunks(n, tasks, workers, [&](int k, int64_t a, int64_t b) {
     uint64_t* h = priv[(size_t)k].data();
     bool r = true;
     switch (dtype) {
@@ -195,15 +211,15 @@ template <typename P, typename C, typename Q>
 void spmv_rows_typed(const P* rp, const C* ci, const double* v, int64_t row0, int64_t row1, const double* x,
                      const Q* perm, double* y, int workers) {
   const int64_t rows = row1 - row0, nz0 = (int64_t)rp[row0], nnz = (int64_t)rp[row1] - nz0;
-  if (rows < 4096 || nnz < (1 << 16)) workers = 1;
-  std::vector<int64_t> cut((size_t)workers + 1);
+  const int tasks = (rows < 4096 || nnz < (1 << 16)) ? 1 : task_count(nnz, workers, 1 << 16);
+  std::vector<int64_t> cut((size_t)tasks + 1);
   cut[0] = row0;
-  cut[(size_t)workers] = row1;
-  for (int k = 1; k < workers; ++k) {  // first row whose start reaches k/w of the nonzeros
-    const int64_t target = nz0 + nnz * k / workers;
+  cut[(size_t)tasks] = row1;
+  for (int k = 1; k < tasks; ++k) {  // first row whose start reaches k/t of the nonzeros
+    const int64_t target = nz0 + nnz * k / tasks;
     cut[(size_t)k] = std::max(cut[(size_t)k - 1], (int64_t)(std::lower_bound(rp + row0, rp + row1, (P)target) - rp));
   }
-  parallel_chunks(workers, workers, [&](int k, int64_t, int64_t) {
+  parallel_chunks(tasks, tasks, workers, [&](int k, int64_t, int64_t) {
     for (int64_t r = cut[(size_t)k]; r < cut[(size_t)k + 1]; ++r) {
       const int64_t e = (int64_t)rp[r + 1];
       double acc = 0.0;
@@ -276,7 +292,8 @@ extern "C" int hb_host_bilateral(const uint8_t* img, int32_t height, int32_t wid
   if (row1 == row0) return HB_OK;
   HB_CHECK_ARG(img && spatial && range256 && out, "NULL pointer");
   const int R = radius, S = 2 * R + 1, W = width, H = height;
-  parallel_chunks(row1 - row0, clamp_workers(workers), [&](int, int64_t a, int64_t b) {
+  workers = clamp_workers(workers);
+  parallel_chunks(row1 - row0, task_count(row1 - row0, workers, 1), workers, [&](int, int64_t a, int64_t b) {
     std::vector<double> num((size_t)W), den((size_t)W);
     for (int64_t rr = a; rr < b; ++rr) {
       const int y = row0 + (int)rr;

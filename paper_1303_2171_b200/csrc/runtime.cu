@@ -87,7 +87,9 @@ class HostPool {
     return *p[which & 1];
   }
   int size() const { return (int)workers_.size() + 1; }
-  void run(const std::function<void(int)>& fn, int n) {
+  // n tasks, claimed dynamically by at most max_threads threads (the caller
+  // included)
+  void run(const std::function<void(int)>& fn, int n, int max_threads = 1 << 30) {
     std::unique_lock<std::mutex> lk(run_mu_);  // one parallel region at a time
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -95,6 +97,7 @@ class HostPool {
       next_ = 0;
       n_ = n;
       done_ = 0;
+      slots_ = std::max(0, std::min(max_threads, n) - 1);
       ++gen_;
     }
     cv_.notify_all();
@@ -120,6 +123,8 @@ class HostPool {
         std::unique_lock<std::mutex> g(mu_);
         cv_.wait(g, [&] { return gen_ != seen && fn_ != nullptr; });
         seen = gen_;
+        if (slots_ <= 0) continue;  // the region has its threads
+        --slots_;
       }
       work();
     }
@@ -143,7 +148,7 @@ class HostPool {
   std::mutex run_mu_, mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;
-  int next_ = 0, n_ = 0, done_ = 0;
+  int next_ = 0, n_ = 0, done_ = 0, slots_ = 0;
   uint64_t gen_ = 0;
 };
 
@@ -294,7 +299,9 @@ bool device_view(void* host, void** dev) {
   return true;
 }
 
-void host_kernel_parallel(int n, const std::function<void(int)>& fn) { HostPool::get(1).run(fn, n); }
+void host_kernel_parallel(int n, const std::function<void(int)>& fn, int max_threads) {
+  HostPool::get(1).run(fn, n, max_threads);
+}
 
 int host_threads() { return HostPool::get().size(); }
 

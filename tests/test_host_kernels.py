@@ -176,3 +176,20 @@ def test_host_spmv_rows_nnz_balanced_and_perm_scatter(idx):
         _host_range_matvec(m, x, 100, 19_000, w, perm=perm, y=y)
         assert np.array_equal(bits(y[perm[100:19_000]]), bits(want[100:19_000]))
         assert np.isnan(np.delete(y, perm[100:19_000])).all()
+
+
+@pytest.mark.parametrize("workers", [1, 2, 15])
+def test_host_histogram_many_tasks(workers):
+    """Inputs large enough to be split into many dynamically claimed tasks
+    (>= 2^18 elements each, up to 16 per worker), with per-task tables capped
+    for wide bin counts: identical to np.bincount, and a bad element in the
+    last task still raises."""
+    rng = np.random.default_rng(11)
+    data = rng.integers(0, 256, size=(1 << 24) + 12345, dtype=np.uint8)
+    assert np.array_equal(host_histogram(data, 256, workers), np.bincount(data, minlength=256))
+    wide = rng.integers(0, 1 << 20, size=(1 << 22) + 7, dtype=np.uint32)
+    assert np.array_equal(host_histogram(wide, 1 << 20, workers), np.bincount(wide, minlength=1 << 20))
+    bad = data.astype(np.int16)
+    bad[-1] = 300
+    with pytest.raises(ValueError):
+        host_histogram(bad, 256, workers)

@@ -9,6 +9,7 @@ streams and `torch.distributed`; every computation is a libhb200 kernel.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 from typing import Any
@@ -128,48 +129,102 @@ def out_like(device: bool, shape: Any, dtype: Any, ref: Any = None) -> Any:
 
 PINNED_MIN_BYTES = 4 << 20
 PINNED_MAX_BYTES = 8 << 30
-PINNED_LIVE_CAP = 4 << 30  # pinned result bytes a caller may hold at once
-
-_pinned_live = [0]  # bytes of pinned results still referenced by callers
-_pinned_lock = __import__("threading").Lock()
+PINNED_POOL_CAP = 8 << 30  # page-locked result blocks the library may make torch cache
 
 
-def _pinned_released(nbytes: int) -> None:
-    with _pinned_lock:
-        _pinned_live[0] -= nbytes
+class _ResultPool:
+    """Bookkeeping of large host results by power-of-two size class (torch's
+    caching host allocator rounds block sizes up to powers of two): which
+    results the caller still holds, how many the caller has dropped, and how
+    many of the library's page-locked result blocks are back in torch's
+    cache, free to be handed out again."""
+
+    def __init__(self):
+        import itertools
+        import threading
+
+        self.lock = threading.Lock()
+        self.keys = itertools.count()
+        self.live: dict[int, tuple[int, Any, bool]] = {}  # key -> (class, scope token, pinned)
+        self.dropped: dict[int, int] = {}  # class -> results the caller let go of
+        self.free: dict[int, int] = {}     # class -> our page-locked blocks back in torch's cache
+        self.pinned_bytes = 0              # page-locked result blocks ever made (torch keeps them)
+
+    def released(self, key: int) -> None:
+        with self.lock:
+            c, _, pinned = self.live.pop(key)
+            self.dropped[c] = self.dropped.get(c, 0) + 1
+            if pinned:
+                self.free[c] = self.free.get(c, 0) + 1
+
+
+_pool = _ResultPool()
+_scope = __import__("threading").local()
+
+
+@contextlib.contextmanager
+def result_scope():
+    """Results allocated inside one scope belong to one API call (e.g. the
+    sorted keys and the payload of gpu_sort): one result of the call being
+    live does not keep the next from being page-locked."""
+    prev = getattr(_scope, "token", None)
+    _scope.token = object()
+    try:
+        yield
+    finally:
+        _scope.token = prev
 
 
 def host_empty(shape: Any, dtype: Any = np.float64) -> np.ndarray:
-    """An uninitialised host array for a result the GPU writes back.  Large
-    results come from torch's caching pinned-host allocator (a numpy view
-    that keeps its block alive; the block returns to the cache when the
-    array is dropped), so the D2H is one DMA straight into the result.  A
-    caller that KEEPS its results would make every call pin fresh memory
-    (cudaHostAlloc: far slower than the copy it saves), so once the live
-    pinned results exceed PINNED_LIVE_CAP further results are plain
-    np.empty (the library copies into them through its pinned stages).
-    Small results, results above PINNED_MAX_BYTES and hosts without CUDA get
-    a plain np.empty too."""
+    """An uninitialised host array for a result the GPU writes back.
+
+    Costs on the B200 box (scripts/prof_pageable.py, per GiB): the D2H into
+    page-locked memory is one DMA (~19 ms); into a fresh pageable array it
+    pays the first-touch zeroing of the pages (~50 ms); pinning FRESH memory
+    (cudaHostAlloc) costs ~450 ms — more than it can save in one call.  So a
+    large result is page-locked only when that is free or pays back:
+      * one of the library's earlier page-locked results of the same size
+        class has been dropped (its block sits in torch's host cache): reuse;
+      * else, the caller has dropped an earlier result of this class and
+        holds none now (a loop that drops each result): pin once — every
+        later call reuses the block;
+      * else (a first call, or a caller that keeps its results): pageable.
+    Results of one API call (`result_scope`) do not hold each other back.
+    Small results, results above PINNED_MAX_BYTES and hosts without CUDA are
+    plain np.empty."""
     import weakref
 
     dt = np.dtype(dtype)
     shape = (int(shape),) if np.ndim(shape) == 0 else tuple(int(d) for d in shape)
     nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
-    if (torch is not None and PINNED_MIN_BYTES <= nbytes <= PINNED_MAX_BYTES and dt in _TORCH_TO_NP.values()
+    if not (torch is not None and PINNED_MIN_BYTES <= nbytes <= PINNED_MAX_BYTES and dt in _TORCH_TO_NP.values()
             and torch.cuda.is_available()):
-        with _pinned_lock:
-            fits = _pinned_live[0] + nbytes <= PINNED_LIVE_CAP
-            if fits:
-                _pinned_live[0] += nbytes
-        if fits:
-            try:
-                arr = torch.empty(shape, dtype=_np_to_torch(dt), pin_memory=True).numpy()
-            except RuntimeError:  # pinned memory exhausted: pageable result
-                _pinned_released(nbytes)
-            else:
-                weakref.finalize(arr, _pinned_released, nbytes)
-                return arr
-    return np.empty(shape, dtype=dt)
+        return np.empty(shape, dtype=dt)
+    c = 1 << (nbytes - 1).bit_length()
+    token = getattr(_scope, "token", None)
+    with _pool.lock:
+        held = any(cc == c and not (token is not None and t is token) for cc, t, _ in _pool.live.values())
+        if _pool.free.get(c, 0) > 0:
+            _pool.free[c] -= 1
+            pin = True
+        elif _pool.dropped.get(c, 0) > 0 and not held and _pool.pinned_bytes + c <= PINNED_POOL_CAP:
+            _pool.pinned_bytes += c
+            pin = True
+        else:
+            pin = False
+        key = next(_pool.keys)
+        _pool.live[key] = (c, token, pin)
+    arr = None
+    if pin:
+        try:
+            arr = torch.empty(shape, dtype=_np_to_torch(dt), pin_memory=True).numpy()
+        except RuntimeError:  # pinned memory exhausted: pageable result
+            with _pool.lock:
+                _pool.live[key] = (c, token, False)
+    if arr is None:
+        arr = np.empty(shape, dtype=dt)
+    weakref.finalize(arr, _pool.released, key)
+    return arr
 
 
 def _np_to_torch(dt: np.dtype):

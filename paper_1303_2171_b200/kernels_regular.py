@@ -21,7 +21,8 @@ import numpy as np
 
 from . import _lib, sharding
 from .errors import DataIOError
-from .gpu import buf, current_stream_handle, flags_for, host_empty, inherit_device, is_device_array, require_gpu, to_host, vp
+from .gpu import (buf, current_stream_handle, flags_for, host_empty, inherit_device, is_device_array, require_gpu,
+                  result_scope, to_host, vp)
 from .platform import Device, DeviceId, Platform
 from .worksharing import WorkShare, formula_share, run_workshared
 
@@ -260,8 +261,9 @@ def gpu_sort(keys: Any, payload: Any = None, *, asynchronous: bool = False,
         k_out, v_out = kb.ptr, (vb.ptr if vb else 0)
         res_k, res_v = keys, payload
     else:
-        res_k = host_empty(kb.owner.shape, kb.dtype)
-        res_v = host_empty(kb.size, vb.dtype) if vb else None
+        with result_scope():
+            res_k = host_empty(kb.owner.shape, kb.dtype)
+            res_v = host_empty(kb.size, vb.dtype) if vb else None
         k_out, v_out = res_k.ctypes.data, (res_v.ctypes.data if vb else 0)
     # asynchronous device sorts do not ask for the pass count: reading it
     # would wait on the digit histogram mid-call (32-bit keys then never

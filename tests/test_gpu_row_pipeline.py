@@ -63,3 +63,59 @@ def test_bilateral_host_pipeline(img, rows):
     for a in (r0, r1 - 2):
         want = obil.rows(img, sp, rg, 4, a, a + 2)
         assert np.array_equal(bits(host[a - r0 : a - r0 + 2]), bits(want))
+
+
+def test_host_empty_pins_only_when_it_pays_back(monkeypatch):
+    """host_empty never makes the library pin fresh memory for a caller that
+    keeps its results: a first result is pageable; once the caller drops a
+    result of a size class (and holds none), the next one is page-locked
+    once and its block is reused by every later call; results of one API
+    call (result_scope) do not hold each other back."""
+    import gc
+
+    import torch
+
+    from paper_1303_2171_b200 import gpu
+    from paper_1303_2171_b200.gpu import host_empty, result_scope
+
+    def pinned(a):
+        return torch.from_numpy(a).is_pinned()
+
+    gc.collect()
+    monkeypatch.setattr(gpu, "_pool", gpu._ResultPool())  # no history from earlier tests
+    n = (1 << 21) + 1000  # 2^25-byte size class
+    a = host_empty(n)
+    assert not pinned(a) and a.shape == (n,) and a.dtype == np.float64  # first result: pageable
+    b = host_empty(n)
+    assert not pinned(b)  # `a` held, nothing dropped yet
+    del a, b
+    gc.collect()
+    c = host_empty(n)  # the caller drops its results: pin once
+    assert pinned(c)
+    d = host_empty(n)  # `c` held: pageable (no fresh pin per call)
+    assert not pinned(d)
+    del c, d
+    gc.collect()
+    e = host_empty(n)  # c's block, reused
+    assert pinned(e)
+    del e
+    gc.collect()
+    with result_scope():
+        k, v = host_empty(n), host_empty(n)
+    assert pinned(k) and pinned(v)
+    del k, v
+    gc.collect()
+    # gpu_sort: keys + payload of one call, dropped between calls
+    from paper_1303_2171_b200.kernels_regular import gpu_sort
+
+    keys = np.random.default_rng(3).integers(0, 1 << 32, size=(1 << 23) + 5, dtype=np.uint32)
+    first = gpu_sort(keys, np.arange(keys.size, dtype=np.uint32))
+    assert np.array_equal(first[0], np.sort(keys)) and np.array_equal(keys[first[1]], first[0])
+    del first
+    gc.collect()
+    for _ in range(2):
+        sk, sv, _ = gpu_sort(keys, np.arange(keys.size, dtype=np.uint32))
+        assert pinned(sk) and pinned(sv)
+        assert np.array_equal(sk, np.sort(keys)) and np.array_equal(keys[sv], sk)
+        del sk, sv
+        gc.collect()

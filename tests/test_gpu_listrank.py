@@ -230,3 +230,35 @@ def test_ballot_ranking_fallback_paths():
     env = dict(os.environ, HB_SORT_RANK="ballot", PYTHONPATH=str(root) + os.pathsep + os.environ.get("PYTHONPATH", ""))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_lists_large(pinned):
+    """Host lists of 2^23+ nodes (many 32 MB pinned-stage chunks, a ragged
+    last chunk), pageable and page-locked int64 successors and int32
+    successors: identical to the device-resident ranking; a successor outside
+    int32 anywhere (first chunk, last element) raises validate_list's range
+    error, and one inside int32 but >= n the same."""
+    import torch
+
+    n = (1 << 23) + 4099
+    seq = np.random.default_rng(7).permutation(n)
+    succ = np.full(n, -1, dtype=np.int64)
+    succ[seq[:-1]] = seq[1:]
+    head = int(seq[0])
+    want = np.empty(n, dtype=np.int64)
+    want[seq] = np.arange(n)
+    if pinned:
+        t = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        t.numpy()[...] = succ
+        succ = t.numpy()
+    got = gpu_list_rank(succ, head)
+    assert got.dtype == np.int64 and np.array_equal(got, want)
+    assert np.array_equal(gpu_list_rank(np.asarray(succ, dtype=np.int32), head), want)
+    dev = gpu_list_rank(torch.from_numpy(np.array(succ)).cuda(), head).cpu().numpy()
+    assert np.array_equal(dev, want)
+    for pos, bad in ((5, 1 << 40), (n - 1, -(1 << 35)), (n // 2, n)):
+        s2 = np.array(succ)
+        s2[seq[pos]] = bad
+        with pytest.raises(StructuralError, match="out of range"):
+            gpu_list_rank(s2, head)

@@ -2,7 +2,7 @@
 # Round-2 closing pass on one B200: full GPU suite + smoke, the N=1 bench line, the reference arm, the
 # 2-rank gloo functional run, the largest shapes, and per-workload ncu evidence (launch lists + one
 # --set full capture of each dominant kernel).  Everything lands in gpurun_out/final/.
-O=gpurun_out/final; mkdir -p $O/prof
+O=gpurun_out/final; rm -rf $O; mkdir -p $O/prof
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $O/smi.txt
 timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -5 > $O/t_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1

@@ -144,6 +144,7 @@ class _ResultPool:
         import threading
 
         self.lock = threading.Lock()
+        self.pending: Any = __import__("collections").deque()  # released keys not yet booked
         self.keys = itertools.count()
         self.live: dict[int, tuple[int, Any, bool]] = {}  # key -> (class, scope token, pinned)
         self.dropped: dict[int, int] = {}  # class -> results the caller let go of
@@ -151,8 +152,15 @@ class _ResultPool:
         self.pinned_bytes = 0              # page-locked result blocks ever made (torch keeps them)
 
     def released(self, key: int) -> None:
-        with self.lock:
-            c, _, pinned = self.live.pop(key)
+        # finalizer: may run inside any allocation, even one made while this
+        # thread holds `lock` (a garbage collection there), so it only queues
+        # the key (deque.append is atomic); book() settles it under the lock
+        self.pending.append(key)
+
+    def book(self) -> None:
+        """Settle queued releases (caller holds `lock`)."""
+        while self.pending:
+            c, _, pinned = self.live.pop(self.pending.popleft())
             self.dropped[c] = self.dropped.get(c, 0) + 1
             if pinned:
                 self.free[c] = self.free.get(c, 0) + 1
@@ -203,6 +211,7 @@ def host_empty(shape: Any, dtype: Any = np.float64) -> np.ndarray:
     c = 1 << (nbytes - 1).bit_length()
     token = getattr(_scope, "token", None)
     with _pool.lock:
+        _pool.book()
         held = any(cc == c and not (token is not None and t is token) for cc, t, _ in _pool.live.values())
         if _pool.free.get(c, 0) > 0:
             _pool.free[c] -= 1
@@ -220,6 +229,7 @@ def host_empty(shape: Any, dtype: Any = np.float64) -> np.ndarray:
             arr = torch.empty(shape, dtype=_np_to_torch(dt), pin_memory=True).numpy()
         except RuntimeError:  # pinned memory exhausted: pageable result
             with _pool.lock:
+                _pool.book()
                 _pool.live[key] = (c, token, False)
     if arr is None:
         arr = np.empty(shape, dtype=dt)

@@ -514,7 +514,8 @@ __global__ void __launch_bounds__(T, MINB)
     onesweep_rfk_kernel(const void* __restrict__ kin_, void* __restrict__ kout_, const uint32_t* __restrict__ vin,
                         uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t flip,
                        const uint32_t* __restrict__ gstart, uint32_t* __restrict__ lookback,
-                       uint32_t* __restrict__ tile_counter, const int64_t* __restrict__ prefix) {
+                       uint32_t* __restrict__ tile_counter, const int64_t* __restrict__ prefix,
+                       uint32_t* __restrict__ clear, uint32_t* __restrict__ clear_counter) {
   static_assert(OUTM == 0 || OUTM == 1, "output split (0) or packed (1)");
   static_assert(INM != 2 || (T * I) % kLogChunkSlots == 0, "log tiles are whole chunks");
   constexpr bool POUT = OUTM == 1;
@@ -537,6 +538,12 @@ __global__ void __launch_bounds__(T, MINB)
   for (int i = tid; i < W * 256; i += T) (&s_base[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
+  // the next pass's look-back words (the other buffer, idle during this
+  // pass) are zeroed tile by tile: no memset kernel between passes
+  if (clear != nullptr && tid < 256) {
+    clear[(size_t)tile * 256 + tid] = 0u;
+    if (tile == 0 && tid == 0) *clear_counter = 0u;
+  }
   const int64_t base = (int64_t)tile * TILE;
   const int valid = (int)min((int64_t)TILE, n - base);
   const int wbase = warp * 32 * I;
@@ -659,6 +666,7 @@ __global__ void atoms_order_check(unsigned int* bad, int rows) {
 struct PassArgs {
   const void* kin; void* kout; const uint32_t* vin; uint32_t* vout;
   int64_t n; int shift; uint64_t flip; const uint32_t* hist; uint32_t* lookback; uint32_t* counter;
+  uint32_t* clear = nullptr; uint32_t* clear_counter = nullptr;  // rfk: the next pass's words, zeroed in-pass
   const uint32_t* gstart;  // pre-scanned digit starts of this pass
   const int64_t* prefix;   // INM 2 (log input): ranked sublist starts
 };
@@ -713,7 +721,7 @@ int launch_rfk(const PassArgs& a, cudaStream_t s, int64_t tiles) {
   auto k = onesweep_rfk_kernel<INM, OUTM, kPkI, kPkT, kPkLbw, kPkMinB>;
   HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<(unsigned)tiles, kPkT, smem, s>>>(a.kin, a.kout, a.vin, a.vout, a.n, a.shift, (uint32_t)a.flip, a.gstart,
-                                        a.lookback, a.counter, a.prefix);
+                                        a.lookback, a.counter, a.prefix, a.clear, a.clear_counter);
   return check_launch();
 }
 
@@ -746,32 +754,58 @@ int launch_pass(const PassArgs& a, bool atoms, cudaStream_t s) {
   return check_launch();
 }
 
+// Look-back words of consecutive onesweep passes: two buffers of `words`
+// (tiles·256 flags + the padded tile counter); pass k uses buffer k % 2 and
+// zeroes the other one tile by tile for pass k + 1, so only the first
+// buffer needs a memset (one per sort instead of one per pass).
+struct LookbackPair {
+  uint32_t* base = nullptr;
+  size_t words = 0;
+  int64_t tiles = 0;
+  void set(int k, bool more, PassArgs& pa) const {
+    uint32_t* cur = base + (size_t)(k & 1) * words;
+    uint32_t* oth = base + (size_t)((k + 1) & 1) * words;
+    pa.lookback = cur;
+    pa.counter = cur + (size_t)tiles * 256;
+    pa.clear = more ? oth : nullptr;
+    pa.clear_counter = more ? oth + (size_t)tiles * 256 : nullptr;
+  }
+};
+
+int lookback_pair(DevBuf& lb, int64_t tiles, LookbackPair* out, cudaStream_t s) {
+  out->tiles = tiles;
+  out->words = (size_t)tiles * 256 + 32;
+  HB_TRY(alloc(&lb, 2 * out->words * 4, s));
+  out->base = lb.as<uint32_t>();
+  HB_CUDA_TRY(cudaMemsetAsync(out->base, 0, out->words * 4, s));
+  return HB_OK;
+}
+
 // live digit passes of a u32-key + u32-payload sort with the pair moved as one
 // 8-byte element: split → packed → … → packed → split (back into keys/vals)
 int packed_passes(uint32_t* keys, uint32_t* vals, int64_t n, uint32_t flip, const bool* live, int nlive,
                   const DevBuf& hist, const DevBuf& gst, DevBuf& lb, cudaStream_t s) {
   const int64_t tiles = ceil_div(n, (int64_t)kPkT * kPkI);
-  const size_t lb_words = (size_t)tiles * 256 + 32;  // + tile counter (padded)
   DevBuf pA, pB;
-  HB_TRY(alloc(&lb, lb_words * 4, s));
+  LookbackPair lbp;
+  HB_TRY(lookback_pair(lb, tiles, &lbp, s));
   HB_TRY(alloc(&pA, (size_t)n * 8, s));
   if (nlive >= 3) HB_TRY(alloc(&pB, (size_t)n * 8, s));
   PassArgs pa{};
   pa.n = n;
-  uint32_t* counter = lb.as<uint32_t>() + (size_t)tiles * 256;
   void* cur = keys;
   void* nxt = pA.ptr;
   int done = 0;
   for (int p = 0; p < 4; ++p) {
     if (!live[p]) continue;
     const bool first = done == 0, last = done == nlive - 1;
-    HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
+    lbp.set(done, !last, pa);
     pa.kin = cur;
     pa.kout = last ? (void*)keys : nxt;
     pa.vin = first ? vals : nullptr;
     pa.vout = last ? vals : nullptr;
     pa.shift = 8 * p; pa.flip = (uint64_t)flip; pa.hist = hist.as<uint32_t>() + p * 256;
-    pa.lookback = lb.as<uint32_t>(); pa.counter = counter; pa.gstart = gst.as<uint32_t>() + p * 256;
+    pa.gstart = gst.as<uint32_t>() + p * 256;
     if (first && last) return HB_EINVAL;  // nlive >= 2 on this path
     if (first) HB_TRY((launch_rfk<0, 1>(pa, s, tiles)));
     else if (last) HB_TRY((launch_rfk<1, 0>(pa, s, tiles)));
@@ -801,21 +835,19 @@ int sort_pairs_bits(uint64_t* pairs, int64_t n, const uint32_t* hist, int shift0
   }
   if (passes < 1 || passes > 4 || shift0 < 0 || shift0 + 8 * passes > 32) return HB_EINVAL;
   const int64_t tiles = ceil_div(n, (int64_t)kPkT * kPkI);
-  const size_t lb_words = (size_t)tiles * 256 + 32;
   DevBuf gst, lb;
   HB_TRY(alloc(&gst, (size_t)passes * 256 * 4, s));
   scan_hist_kernel<<<passes, 256, 0, s>>>(hist, gst.as<uint32_t>(), passes);
   HB_TRY(check_launch());
-  HB_TRY(alloc(&lb, lb_words * 4, s));
+  LookbackPair lbp;
+  HB_TRY(lookback_pair(lb, tiles, &lbp, s));
   PassArgs pa{};
   pa.n = n;
   pa.flip = 0;
-  pa.lookback = lb.as<uint32_t>();
-  pa.counter = lb.as<uint32_t>() + (size_t)tiles * 256;
   void* cur = pairs;
   void* nxt = alt;
   for (int p = 0; p < passes; ++p) {
-    HB_CUDA_TRY(cudaMemsetAsync(lb.ptr, 0, lb_words * 4, s));
+    lbp.set(p, p + 1 < passes, pa);
     pa.kin = cur;
     pa.kout = nxt;
     pa.vin = nullptr;

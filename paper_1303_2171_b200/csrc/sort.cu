@@ -711,9 +711,11 @@ bool use_atomics_rank(int flags) {
 }
 
 // u32 key + u32 payload moved as one 8-byte element: 22 keys/thread, 256
-// threads, 3 CTAs/SM, look-back window 2 (measured best: 59.5 Gkeys/s;
-// 24: 57.4, 20: 55.6)
-constexpr int kPkI = 22, kPkT = 256, kPkLbw = 2, kPkMinB = 3;
+// threads, 3 CTAs/SM (measured best: 59.5 Gkeys/s; 24: 57.4, 20: 55.6);
+// look-back window 3 predecessors per round trip (2^28 pairs: window 1 / 2 /
+// 3 / 4 / 5 / 6 = 4.75 / 4.36 / 4.29 / 4.32 / 4.34 / 4.38 ms,
+// profiles/micro_sort_lookback_reset_r02.txt)
+constexpr int kPkI = 22, kPkT = 256, kPkLbw = 3, kPkMinB = 3;
 
 template <int INM, int OUTM>
 int launch_rfk(const PassArgs& a, cudaStream_t s, int64_t tiles) {

@@ -742,7 +742,7 @@ int launch_pass(const PassArgs& a, bool atoms, cudaStream_t s) {
   const int64_t tiles = Sh::tiles(a.n, atoms);
   if (atoms) {
     const size_t smem = (size_t)Sh::rf_t * Sh::rf_i * (sizeof(K) + (HAS_V ? 4 : 0));
-    auto k = onesweep_rf_kernel<K, HAS_V, Sh::rf_i, Sh::rf_t, 2, 3, true>;
+    auto k = onesweep_rf_kernel<K, HAS_V, Sh::rf_i, Sh::rf_t, 3, 3, true>;  // look-back window 3 (as the packed pass)
     HB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<(unsigned)tiles, Sh::rf_t, smem, s>>>((const K*)a.kin, (K*)a.kout, a.vin, a.vout, a.n, a.shift, (K)a.flip,
                                               a.gstart, a.lookback, a.counter);

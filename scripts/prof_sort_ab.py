@@ -32,6 +32,20 @@ k64 = keys.view(torch.int32).long() & 0xFFFFFFFF
 ok = bool((k64[1:] >= k64[:-1]).all()) and bool((src.view(torch.int32)[vals.view(torch.int32).long()] == keys.view(torch.int32)).all())
 lib = os.environ.get("HB200_LIB", "default").split("/")[-1]
 print(f"{lib:22s} sort 2^28 pairs: {sum(ts) / len(ts):.3f} ms  ({n / (sum(ts) / len(ts)) / 1e6:.0f} Mkeys/s) ok={ok}", flush=True)
+for name, dt in (("keys-only u32", torch.int32), ("keys-only u64", torch.int64)):
+    ks = torch.randint(0, 1 << 62, (n // (2 if dt == torch.int64 else 1),), device="cuda", dtype=torch.int64,
+                       generator=g).to(dt)
+    kk = torch.empty_like(ks)
+    ts = []
+    for i in range(8):
+        kk.copy_(ks)
+        e0.record()
+        gpu_sort(kk, None, asynchronous=True)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    print(f"{lib:22s} sort {name} ({kk.numel()} keys): {sum(ts) / len(ts):.3f} ms", flush=True)
 succ, head = device_gen_list(n, 42)
 r = torch.empty(n, dtype=torch.int64, device="cuda")
 ts = []

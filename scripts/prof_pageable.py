@@ -63,7 +63,19 @@ def fill_fresh():
     r.fill(1)
 
 
+def down_fresh_4k():
+    from numpy._core import multiarray as ma
+
+    prev = ma._set_madvise_hugepage(False)  # numpy madvises large arrays MADV_HUGEPAGE by default
+    try:
+        r = np.empty(n, dtype=np.uint8)
+    finally:
+        ma._set_madvise_hugepage(prev)
+    _lib.call("hb_buf_download", vp(r.ctypes.data), vp(d.data_ptr()), n, 0, vp(0))
+
+
 for name, fn in [("upload pageable (touched)", up), ("download into touched", down_touched),
+                 ("download into fresh np.empty, 4 KB pages", down_fresh_4k),
                  ("download into fresh np.empty", down_fresh), ("first touch only (1 byte/page, 1 thread)", touch_fresh),
                  ("fill fresh np.empty (1 thread)", fill_fresh)]:
     mn, md = t(fn)

@@ -193,3 +193,22 @@ def test_host_histogram_many_tasks(workers):
     bad[-1] = 300
     with pytest.raises(ValueError):
         host_histogram(bad, 256, workers)
+
+
+def test_result_pool_bookkeeping():
+    """gpu._ResultPool (host_empty's pinned-result policy) on its own, no GPU:
+    releases queue lock-free and are settled on the next booking; a release
+    counts as a drop of its size class, and a pinned one frees its block."""
+    from paper_1303_2171_b200.gpu import _ResultPool
+
+    pool = _ResultPool()
+    c = 1 << 25
+    with pool.lock:
+        pool.live[1] = (c, None, False)
+        pool.live[2] = (c, None, True)
+    pool.released(1)
+    pool.released(2)  # finalizers: queued only
+    assert len(pool.live) == 2 and pool.dropped == {} and pool.free == {}
+    with pool.lock:
+        pool.book()
+    assert pool.live == {} and pool.dropped == {c: 2} and pool.free == {c: 1}
